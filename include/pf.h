@@ -1,0 +1,163 @@
+/* pf.h — C ABI of libpf.so, the B200 (sm_100a) explicit time step of the
+ * grand-potential phase-field model for ternary eutectic directional
+ * solidification (Bauer et al., SC'15, arXiv 1506.01684).
+ *
+ * One call of pf_step(ctx, 1) is Algorithm 1 of the paper (PAPER.md:158-174,
+ * §Phase-field Algorithm):
+ *     phi_dst <- phi-kernel(phi_src, mu_src)           Eq. (1)-(2)
+ *     phi_dst ghost-layer exchange + boundary handling
+ *     mu_dst  <- mu-kernel(mu_src, phi_src, phi_dst)   Eq. (3)-(4)
+ *     mu_dst  ghost-layer exchange + boundary handling
+ *     swap src <-> dst
+ * followed, when enabled, by the moving-window shift.  The
+ * problem statement the entry points follow is pf_create(grid, params),
+ * pf_init(seed), pf_step(n), pf_read(phi, mu) (BASELINE.json north_star).
+ *
+ * Conventions
+ *  - Fields are IEEE binary64 ("all computations are carried out
+ *    in double precision").  Phases a = 0..3 = alpha, beta, gamma, liquid
+ *    (N = 4); chemical potentials c = 0,1 (K-1 = 2).
+ *  - Host-visible layout of a state (pf_read / pf_write): the rank's local
+ *    interior box only, structure of arrays, x fastest:
+ *        phi[a*n + (k*ny_l + j)*nx_l + i],  mu[c*n + (k*ny_l + j)*nx_l + i],
+ *    n = nx_l*ny_l*nz_l.  Pointers may be host or device memory (detected).
+ *  - Boundaries: periodic in x and y, zero-flux (zero-gradient ghosts) in z.
+ *  - Every function returns pf_status; no C++ exception crosses the ABI.  After
+ *    any error the context is poisoned: later calls return PF_ERR_STATE, and
+ *    pf_last_error() describes the first failure.  A context is
+ *    single-thread-affine.
+ *  - Ownership: the context owns every device allocation (fields, halo
+ *    buffers, per-plane table, events) and the NCCL communicator it creates.
+ *    The caller owns the structs passed to pf_create (copied) and the buffers
+ *    passed to pf_read / pf_write.  A borrowed stream must outlive the context.
+ */
+#ifndef PF_H_
+#define PF_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PF_OK = 0,
+  PF_ERR_CONFIG = -1,    /* invalid grid / decomposition / parameters            */
+  PF_ERR_NUMERICAL = -2, /* NaN or Inf found by the periodic device check          */
+  PF_ERR_CUDA = -3,      /* a CUDA runtime error (message in pf_last_error)        */
+  PF_ERR_COMM = -4,      /* an NCCL error                                          */
+  PF_ERR_STATE = -5,     /* call out of order (step before init) or after an error */
+  PF_ERR_ARG = -6        /* NULL or out-of-range argument                          */
+} pf_status;
+
+/* Grid and decomposition (copied by pf_create).  The global nx*ny*nz interior
+ * is split into px*py*pz equal blocks (nx % px == 0 etc., else PF_ERR_CONFIG
+ * naming the axis).  Block b = ix + px*(iy + py*iz).  Either
+ * nranks == 1 (all blocks on this GPU; blocks exchange halos in device memory)
+ * or nranks == px*py*pz (block b on rank b, halos over NCCL send/recv). */
+typedef struct {
+  int64_t nx, ny, nz;
+  int32_t px, py, pz;
+  int32_t rank, nranks;
+  int32_t device;        /* CUDA ordinal of this process's GPU                     */
+  uint8_t nccl_id[128];  /* ncclUniqueId from pf_nccl_unique_id() on rank 0,
+                            broadcast by the caller (torch.distributed); ignored
+                            when nranks == 1                                      */
+  void *stream;          /* cudaStream_t to run on, or NULL for a library stream   */
+} pf_grid;
+
+/* Model parameters (copied).  Symbols of PAPER.md Eq. (1)-(4); their values
+ * are not in the paper (PAPER.md:197 defers to [hoetzer15]); params/v1.json is
+ * the builder's PARAMS-v1 set. */
+typedef struct {
+  double dx, dt, eps;         /* grid spacing, time step, interface parameter eps  */
+  double tau[4];              /* relaxation tau_a (Eq. 1)                          */
+  double gamma[4][4];         /* pairwise gradient/obstacle coefficient gamma_ab   */
+  double gamma3[4];           /* higher-order obstacle coefficient of the triple
+                                 that EXCLUDES phase x (x = 3: alpha-beta-gamma)   */
+  double delta[4][4];         /* cubic anisotropy strength of pair ab (aniso only) */
+  double T_eut, G, v, T0;     /* frozen T(z,t) = T0 + G (z - v t)  */
+  double A0[4][2], A1[4][2];  /* parabola curvature A = A0 + A1 (T - T_eut)        */
+  double c0[4][2], m[4][2];   /* c-hat = c0 + m (T - T_eut)                        */
+  double L[4];                /* driving offset B = L (T - T_eut) / T_eut          */
+  double D[4][2];             /* diffusivities (mobility M = sum phi D / 2A)       */
+  int32_t aniso;              /* 0: isotropic gradient energy (D3C7); 1: cubic
+                                 anisotropy (D3C19 phi stencil)                     */
+  int32_t window;             /* 1: moving window along z           */
+  double window_frac;         /* shift when the front reaches ceil(frac * NZ)      */
+  double window_phi_l;        /* front = highest plane with some phi_l < this      */
+  int32_t nan_check_every;    /* check phi/mu for NaN/Inf every k steps (0 = off)  */
+  int32_t variant;            /* 0: tiled kernels (default); 1: naive per-cell
+                                 kernels (every face evaluated from both cells)     */
+  /* initial condition recipe for pf_init */
+  int32_t init_kind;          /* 0 voronoi, 1 lamellar, 2 planar                   */
+  int32_t init_n_seeds;
+  int32_t init_lam_wmin, init_lam_wmax, init_planar_phase, pad_;
+  double init_layer_height, init_iface_width, init_mu_noise;
+} pf_params;
+
+/* Run-time information about a context. */
+typedef struct {
+  int64_t nx_l, ny_l, nz_l;   /* this rank's interior box                          */
+  int64_t x0, y0, z0;         /* its global offset                                 */
+  int64_t step;               /* time level n of the current state                 */
+  int64_t z_origin;           /* moving-window origin (global plane of k = 0)      */
+  int64_t shifts;             /* window shifts so far                              */
+  int64_t last_front;         /* last front plane seen (-1: none / not computed)   */
+  int32_t nblocks_local;
+  int32_t timing;             /* 1 if per-sweep timing is enabled                  */
+  double ms_phi, ms_mu, ms_halo, ms_other; /* accumulated device time per kernel
+                                 family (CUDA events on the launching stream)      */
+  int64_t launches;           /* kernels launched by pf_step so far                */
+  int64_t phi_launches, mu_launches; /* sweep launches counted in ms_phi / ms_mu   */
+} pf_info_t;
+
+typedef struct pf_ctx pf_ctx;
+
+/* Fill out[128] with a fresh ncclUniqueId (call on rank 0 only). */
+pf_status pf_nccl_unique_id(uint8_t out[128]);
+
+/* Validate grid and parameters, select the device, allocate fields and
+ * buffers, create the communicator (nranks > 1; collective over all ranks).
+ * Errors: PF_ERR_CONFIG (divisibility, gamma not symmetric / non-positive,
+ * A(T) <= 0 within the run's temperature range), PF_ERR_ARG, PF_ERR_CUDA,
+ * PF_ERR_COMM.  On success *out owns everything. */
+pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out);
+
+/* Deterministic, decomposition-independent initial state from `seed` and the
+ * init_* recipe (Voronoi / lamellar / planar solid layer under liquid,
+ * PAPER.md:195-197), generated on the device; resets step and z_origin to 0
+ * and fills all ghosts. */
+pf_status pf_init(pf_ctx *c, uint64_t seed);
+
+/* Load a state (layout above; host or device pointers), fill all ghosts. */
+pf_status pf_write(pf_ctx *c, const double *phi, const double *mu);
+
+/* Set the time level n (t = n dt) and the window origin of the current state. */
+pf_status pf_set_time(pf_ctx *c, int64_t step, int64_t z_origin);
+
+/* Advance n explicit steps (Algorithm 1 + window).  Blocking: returns after
+ * the last step completed on the device.  Errors: PF_ERR_STATE before
+ * pf_init/pf_write, PF_ERR_NUMERICAL with step, global cell and field in
+ * pf_last_error when the NaN check trips, PF_ERR_CUDA / PF_ERR_COMM. */
+pf_status pf_step(pf_ctx *c, int64_t n);
+
+/* Copy the rank's interior state out (layout above; host or device). */
+pf_status pf_read(pf_ctx *c, double *phi, double *mu);
+
+/* Enable (1) / disable (0) per-sweep CUDA-event timing; resets the timers. */
+pf_status pf_set_timing(pf_ctx *c, int32_t on);
+
+pf_status pf_info(pf_ctx *c, pf_info_t *out);
+
+/* Message describing the first error on c (or a create failure when c is
+ * NULL); valid until the next call on c. */
+const char *pf_last_error(const pf_ctx *c);
+
+/* Release every resource; c may be NULL. */
+void pf_destroy(pf_ctx *c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PF_H_ */

@@ -1,0 +1,324 @@
+// pf_dev.cuh — device-side model arithmetic of the phi- and mu-sweeps
+// (Eq. (1)-(4), lines 89-135; readings R1-R25 of DESIGN.md §2).
+//
+// Rounding discipline: every quantity that two different threads / code
+// locations must reproduce bit for bit — a face flux (PAPER.md:299-317
+// "staggered positions"), the per-cell quantities the faces are built from,
+// the centre gradients — is written with explicit round-to-nearest intrinsics
+// (__dadd_rn / __dmul_rn / __fma_rn ...), so nvcc cannot contract it
+// differently at different call sites.  This gives (i) exact telescoping of the
+// flux-form divergence (solute conservation, DESIGN.md pin P4) and (ii) bitwise
+// decomposition invariance (P9): a face evaluated at a tile or block edge has
+// the same bits as the same face evaluated mid-tile.  Cell-local updates are
+// free for the compiler to contract.
+#pragma once
+#include <cstdint>
+
+namespace pf {
+
+constexpr int NPH = 4;   // phases alpha, beta, gamma, liquid
+constexpr int NMU = 2;   // independent chemical potentials (K-1)
+constexpr int LIQ = 3;
+
+// pair index p of (a<b): (0,1)=0 (0,2)=1 (0,3)=2 (1,2)=3 (1,3)=4 (2,3)=5
+__host__ __device__ constexpr int pair_a(int p) { return p < 3 ? 0 : (p < 5 ? 1 : 2); }
+__host__ __device__ constexpr int pair_b(int p) { return p < 3 ? p + 1 : (p < 5 ? p - 1 : 3); }
+
+// Per-step constants (kernel argument, lives in the constant bank).
+struct KParams {
+  double dt, inv_dt, inv_dx, inv_2dx, half_inv_dt;
+  double dt_taueps[NPH];   // dt / (tau_a eps)
+  double g2[6];            // 2 gamma_ab per pair
+  double delta[6];         // cubic anisotropy per pair
+  double om[NPH][NPH];     // 16/pi^2 gamma_ab (0 on the diagonal)
+  double g3[NPH];          // triple coefficient of the triple excluding x
+  double pi_eps_4;         // pi eps / 4
+  double Gv;               // G v = -dT/dt
+  int aniso;
+};
+
+// Per-plane table (T-only subexpressions once per
+// x-y slice).  TAB doubles per plane, index = global window plane + 1.
+enum {
+  T_T = 0, T_EPST = 1, T_TEPS = 2,
+  T_INV2A = 3,    // + a*2 + c   1/(2A)
+  T_CHAT = 11,    // + a*2 + c   c-hat
+  T_INV4A = 19,   // + a*2 + c   1/(4A)
+  T_KAPPA = 27,   // + a*2 + c   2 A1 / (2A)^2
+  T_MC = 35,      // + a*2 + c   D / (2A)
+  T_B = 43,       // + a         L (T - T_eut) / T_eut
+  T_MCHAT = 47,   // + a*2+c     m (as given; constant, kept for locality)
+  TAB = 56
+};
+
+#define RN_ADD __dadd_rn
+#define RN_SUB __dsub_rn
+#define RN_MUL __dmul_rn
+#define RN_FMA __fma_rn
+
+// ---------------------------------------------------------------------------
+// phi-sweep
+// ---------------------------------------------------------------------------
+
+// Cubic-anisotropy gradient of the pair energy e = gamma a_c^2 |q|^2,
+// a_c = 1 - delta (3 - 4 Q4/|q|^4) (reading R3); g = 0 at q = 0.
+// Pinned: used inside face fluxes.  Returns g (without the 2 gamma factor
+// folded: full g).
+__device__ __forceinline__ void pair_grad_aniso(double g2, double delta, const double q[3], double out[3]) {
+  const double q2 = RN_FMA(q[2], q[2], RN_FMA(q[1], q[1], RN_MUL(q[0], q[0])));
+  if (q2 == 0.0) { out[0] = out[1] = out[2] = 0.0; return; }
+  double s2[3], s4 = 0.0;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) { s2[d] = RN_MUL(q[d], q[d]); }
+  s4 = RN_FMA(s2[2], s2[2], RN_FMA(s2[1], s2[1], RN_MUL(s2[0], s2[0])));   // Q4
+  const double r2 = __drcp_rn(q2);
+  const double r4 = RN_MUL(r2, r2);
+  const double x = RN_MUL(s4, r4);                                          // Q4/|q|^4
+  const double ac = RN_SUB(1.0, RN_MUL(delta, RN_FMA(-4.0, x, 3.0)));       // a_c
+  // |q|^2 d a_c/d q_d = 16 delta (q_d^3 - Q4 q_d / |q|^2) / |q|^2
+  const double d16 = RN_MUL(16.0, delta);
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double t = RN_MUL(RN_FMA(s2[d], q[d], -RN_MUL(RN_MUL(s4, r2), q[d])), r2);
+    out[d] = RN_MUL(RN_MUL(g2, ac), RN_FMA(d16, t, RN_MUL(ac, q[d])));
+  }
+}
+
+// Face flux j_a (component d) of the phi-sweep between cells lo and hi = lo+e_d
+// (oracle O4.5): phibar = (lo+hi)/2, normal gradient (hi-lo)/dx, tangential
+// gradient = mean of the two centre gradients (anisotropic only);
+// j_a = -sum_{b != a} g_ab,d(q_ab) phibar_b.  Pinned rounding.
+__device__ __forceinline__ void phi_face(const KParams &kp, const double plo[NPH], const double phi_[NPH],
+                                         const double glo[NPH][3], const double ghi[NPH][3], int d,
+                                         double jf[NPH]) {
+  double pb[NPH], gn[NPH];
+#pragma unroll
+  for (int a = 0; a < NPH; ++a) {
+    pb[a] = RN_MUL(0.5, RN_ADD(plo[a], phi_[a]));
+    gn[a] = RN_MUL(RN_SUB(phi_[a], plo[a]), kp.inv_dx);
+    jf[a] = 0.0;
+  }
+  if (!kp.aniso) {
+#pragma unroll
+    for (int p = 0; p < 6; ++p) {
+      const int a = pair_a(p), b = pair_b(p);
+      const double G = RN_MUL(kp.g2[p], RN_FMA(pb[a], gn[b], -RN_MUL(pb[b], gn[a])));
+      jf[a] = RN_FMA(-G, pb[b], jf[a]);
+      jf[b] = RN_FMA(G, pb[a], jf[b]);
+    }
+  } else {
+    double gf[NPH][3];
+#pragma unroll
+    for (int a = 0; a < NPH; ++a)
+#pragma unroll
+      for (int e = 0; e < 3; ++e)
+        gf[a][e] = (e == d) ? gn[a] : RN_MUL(0.5, RN_ADD(glo[a][e], ghi[a][e]));
+#pragma unroll
+    for (int p = 0; p < 6; ++p) {
+      const int a = pair_a(p), b = pair_b(p);
+      double q[3], g[3];
+#pragma unroll
+      for (int e = 0; e < 3; ++e) q[e] = RN_FMA(pb[a], gf[b][e], -RN_MUL(pb[b], gf[a][e]));
+      if (kp.delta[p] == 0.0) {
+#pragma unroll
+        for (int e = 0; e < 3; ++e) g[e] = RN_MUL(kp.g2[p], q[e]);
+      } else {
+        pair_grad_aniso(kp.g2[p], kp.delta[p], q, g);
+      }
+      jf[a] = RN_FMA(-g[d], pb[b], jf[a]);
+      jf[b] = RN_FMA(g[d], pb[a], jf[b]);
+    }
+  }
+}
+
+// Centre gradient (hi - lo) / (2 dx), pinned.
+__device__ __forceinline__ double cgrad(const KParams &kp, double lo, double hi) {
+  return RN_MUL(RN_SUB(hi, lo), kp.inv_2dx);
+}
+
+// Cell part of the phi update (oracle O4.1-4.11) given the cell value, its
+// chemical potential, centre gradients, the 6 face fluxes (jm: lower faces,
+// jp: upper faces, per direction) and the plane's table row.
+__device__ __forceinline__ void phi_cell_update(const KParams &kp, const double *__restrict__ tab,
+                                                const double ph[NPH], const double mu[NMU],
+                                                const double gc[NPH][3], const double jm[3][NPH],
+                                                const double jp[3][NPH], double out[NPH]) {
+  // d a / d phi_a = sum_{b != a} g_ab(q_ab) . grad phi_b   (O4.2-4)
+  double dad[NPH] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int p = 0; p < 6; ++p) {
+    const int a = pair_a(p), b = pair_b(p);
+    double q[3], g[3];
+#pragma unroll
+    for (int e = 0; e < 3; ++e) q[e] = ph[a] * gc[b][e] - ph[b] * gc[a][e];
+    if (kp.aniso && kp.delta[p] != 0.0) {
+      pair_grad_aniso(kp.g2[p], kp.delta[p], q, g);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 3; ++e) g[e] = kp.g2[p] * q[e];
+    }
+    dad[a] += g[0] * gc[b][0] + g[1] * gc[b][1] + g[2] * gc[b][2];
+    dad[b] -= g[0] * gc[a][0] + g[1] * gc[a][1] + g[2] * gc[a][2];
+  }
+  // thermodynamics of the plane: psi_a = B_a - sum_c mu_c (mu_c/(4A) + chat)
+  double ps[NPH];
+#pragma unroll
+  for (int a = 0; a < NPH; ++a) {
+    double s = tab[T_B + a];
+#pragma unroll
+    for (int c = 0; c < NMU; ++c) s -= mu[c] * (mu[c] * tab[T_INV4A + a * 2 + c] + tab[T_CHAT + a * 2 + c]);
+    ps[a] = s;
+  }
+  const double S = ph[0] * ph[0] + ph[1] * ph[1] + ph[2] * ph[2] + ph[3] * ph[3];
+  const double rS = 1.0 / S;
+  const double pbar = rS * (ph[0] * ph[0] * ps[0] + ph[1] * ph[1] * ps[1] + ph[2] * ph[2] * ps[2] +
+                            ph[3] * ph[3] * ps[3]);
+  const double epsT = tab[T_EPST], Teps = tab[T_TEPS];
+  double rhs[NPH], sum = 0.0;
+#pragma unroll
+  for (int a = 0; a < NPH; ++a) {
+    // O4.6 divergence of the face fluxes
+    const double div = ((jp[0][a] - jm[0][a]) + (jp[1][a] - jm[1][a]) + (jp[2][a] - jm[2][a])) * kp.inv_dx;
+    // O4.7 multi-obstacle derivative
+    double om = 0.0;
+#pragma unroll
+    for (int b = 0; b < NPH; ++b) if (b != a) om += kp.om[a][b] * ph[b];
+#pragma unroll
+    for (int x = 0; x < NPH; ++x) {
+      if (x == a) continue;
+      int b = -1, e = -1;
+#pragma unroll
+      for (int y = 0; y < NPH; ++y) if (y != a && y != x) { if (b < 0) b = y; else e = y; }
+      om += kp.g3[x] * ph[b] * ph[e];
+    }
+    // O4.8 driving force
+    const double dpsi = 2.0 * ph[a] * rS * (ps[a] - pbar);
+    rhs[a] = epsT * (dad[a] - div) + Teps * om + dpsi;     // O4.9
+    sum += rhs[a];
+  }
+  const double mean = 0.25 * sum;
+  double x[NPH];
+#pragma unroll
+  for (int a = 0; a < NPH; ++a) x[a] = ph[a] - kp.dt_taueps[a] * (rhs[a] - mean);   // O4.10 (minus sign, R1)
+
+  // O4.11 Euclidean projection onto the simplex: sort descending (network),
+  // theta = (sum of the rho largest - 1)/rho with rho the largest j such that
+  // u_j > (sum_{r<=j} u_r - 1)/j.
+  double u0 = x[0], u1 = x[1], u2 = x[2], u3 = x[3], t;
+#define PF_CSWAP(p, q) if (p < q) { t = p; p = q; q = t; }
+  PF_CSWAP(u0, u1) PF_CSWAP(u2, u3) PF_CSWAP(u0, u2) PF_CSWAP(u1, u3) PF_CSWAP(u1, u2)
+#undef PF_CSWAP
+  const double c1 = u0 - 1.0, c2 = c1 + u1, c3 = c2 + u2, c4 = c3 + u3;
+  const double t1 = c1, t2 = 0.5 * c2, t3 = c3 / 3.0, t4 = 0.25 * c4;
+  double theta = t1;
+  if (u1 - t2 > 0.0) theta = t2;
+  if (u2 - t3 > 0.0) theta = t3;
+  if (u3 - t4 > 0.0) theta = t4;
+#pragma unroll
+  for (int a = 0; a < NPH; ++a) out[a] = fmax(x[a] - theta, 0.0);
+}
+
+// ---------------------------------------------------------------------------
+// mu-sweep
+// ---------------------------------------------------------------------------
+
+// Per-cell quantities a mu face needs (oracle MuCellQ), pinned.
+struct MuQ {
+  double pn[NPH];     // phi^{n+1}
+  double dp[NPH];     // phi^{n+1} - phi^n
+  double gn[NPH][3];  // centre gradient of phi^{n+1} (tangential parts used)
+  double M[NMU];      // sum_a phi^n_a D/(2A)          (R11)
+  double dcl[3][NMU]; // c^l - c^a for the solids a   (R10)
+  double mu[NMU];
+};
+
+__device__ __forceinline__ void mu_cell_q(const double *__restrict__ tab, const double po[NPH],
+                                          const double pn[NPH], const double mu[NMU], MuQ &q) {
+#pragma unroll
+  for (int a = 0; a < NPH; ++a) { q.pn[a] = pn[a]; q.dp[a] = RN_SUB(pn[a], po[a]); }
+#pragma unroll
+  for (int c = 0; c < NMU; ++c) {
+    q.mu[c] = mu[c];
+    double M = RN_MUL(po[0], tab[T_MC + 0 * 2 + c]);
+    M = RN_FMA(po[1], tab[T_MC + 1 * 2 + c], M);
+    M = RN_FMA(po[2], tab[T_MC + 2 * 2 + c], M);
+    M = RN_FMA(po[3], tab[T_MC + 3 * 2 + c], M);
+    q.M[c] = M;
+    // c^a = mu * inv2A + chat;  c^l - c^a
+    const double cl = RN_FMA(mu[c], tab[T_INV2A + LIQ * 2 + c], tab[T_CHAT + LIQ * 2 + c]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      q.dcl[a][c] = RN_SUB(cl, RN_FMA(mu[c], tab[T_INV2A + a * 2 + c], tab[T_CHAT + a * 2 + c]));
+  }
+}
+
+// (M grad mu - J_at)_c at the face (lo, hi = lo + e_d) — oracle mu_face.
+// Pinned rounding; guards are exact-zero tests (reading R10).
+__device__ __forceinline__ void mu_face(const KParams &kp, const MuQ &lo, const MuQ &hi, int d, double out[NMU]) {
+#pragma unroll
+  for (int c = 0; c < NMU; ++c)
+    out[c] = RN_MUL(RN_MUL(RN_MUL(0.5, RN_ADD(lo.M[c], hi.M[c])), RN_SUB(hi.mu[c], lo.mu[c])), kp.inv_dx);
+  double pb[NPH], gf[NPH][3];
+#pragma unroll
+  for (int a = 0; a < NPH; ++a) {
+    pb[a] = RN_MUL(0.5, RN_ADD(lo.pn[a], hi.pn[a]));
+#pragma unroll
+    for (int e = 0; e < 3; ++e)
+      gf[a][e] = (e == d) ? RN_MUL(RN_SUB(hi.pn[a], lo.pn[a]), kp.inv_dx)
+                          : RN_MUL(0.5, RN_ADD(lo.gn[a][e], hi.gn[a][e]));
+  }
+  const double gl2 = RN_FMA(gf[LIQ][2], gf[LIQ][2], RN_FMA(gf[LIQ][1], gf[LIQ][1], RN_MUL(gf[LIQ][0], gf[LIQ][0])));
+  if (pb[LIQ] == 0.0 || gl2 == 0.0) return;     // no liquid / flat liquid: J = 0
+  const double S = RN_FMA(pb[3], pb[3], RN_FMA(pb[2], pb[2], RN_FMA(pb[1], pb[1], RN_MUL(pb[0], pb[0]))));
+  const double hl = __ddiv_rn(RN_MUL(pb[LIQ], pb[LIQ]), S);
+  const double rl = rsqrt(gl2);
+  double J0 = 0.0, J1 = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double pal = RN_MUL(pb[a], pb[LIQ]);
+    const double ga2 = RN_FMA(gf[a][2], gf[a][2], RN_FMA(gf[a][1], gf[a][1], RN_MUL(gf[a][0], gf[a][0])));
+    const double pd = RN_MUL(RN_ADD(lo.dp[a], hi.dp[a]), kp.half_inv_dt);
+    if (pal == 0.0 || ga2 == 0.0 || pd == 0.0) continue;
+    const double ra = rsqrt(ga2);
+    const double dot = RN_FMA(gf[a][2], gf[LIQ][2], RN_FMA(gf[a][1], gf[LIQ][1], RN_MUL(gf[a][0], gf[LIQ][0])));
+    // (pi eps/4) phi_a h_l / sqrt(phi_a phi_l) * dphi_a/dt * (n_a . n_l) * n_a,d
+    const double w = RN_MUL(RN_MUL(RN_MUL(RN_MUL(kp.pi_eps_4, RN_MUL(RN_MUL(pb[a], hl), rsqrt(pal))), pd),
+                                   RN_MUL(RN_MUL(dot, ra), rl)),
+                            RN_MUL(gf[a][d], ra));
+    J0 = RN_FMA(w, RN_MUL(0.5, RN_ADD(lo.dcl[a][0], hi.dcl[a][0])), J0);
+    J1 = RN_FMA(w, RN_MUL(0.5, RN_ADD(lo.dcl[a][1], hi.dcl[a][1])), J1);
+  }
+  out[0] = RN_SUB(out[0], J0);
+  out[1] = RN_SUB(out[1], J1);
+}
+
+// Cell part of the mu update (oracle O5.1-5.9) given phi^n, phi^{n+1}, mu^n of
+// the cell, the divergence sum_d (f^+ - f^-) of the face values, and the table.
+__device__ __forceinline__ void mu_cell_update(const KParams &kp, const double *__restrict__ tab,
+                                               const double po[NPH], const double pn[NPH], const double mu[NMU],
+                                               const double divf[NMU], double out[NMU]) {
+  const double So = po[0] * po[0] + po[1] * po[1] + po[2] * po[2] + po[3] * po[3];
+  const double Sn = pn[0] * pn[0] + pn[1] * pn[1] + pn[2] * pn[2] + pn[3] * pn[3];
+  const double rSo = 1.0 / So, rSn = 1.0 / Sn;
+  double hn[NPH], dh[NPH];
+#pragma unroll
+  for (int a = 0; a < NPH; ++a) {
+    hn[a] = pn[a] * pn[a] * rSn;
+    dh[a] = hn[a] - po[a] * po[a] * rSo;
+  }
+#pragma unroll
+  for (int c = 0; c < NMU; ++c) {
+    double chi = 0.0, s = 0.0, dcdT = 0.0;
+#pragma unroll
+    for (int a = 0; a < NPH; ++a) {
+      const double i2a = tab[T_INV2A + a * 2 + c];
+      chi += hn[a] * i2a;                                                  // O5.3
+      s += (mu[c] * i2a + tab[T_CHAT + a * 2 + c]) * dh[a];                // O5.4 (sign below)
+      dcdT += hn[a] * (tab[T_MCHAT + a * 2 + c] - mu[c] * tab[T_KAPPA + a * 2 + c]);  // O5.5
+    }
+    // mu^{n+1} = mu + dt/chi [ -s/dt + dcdT G v + div ]
+    out[c] = mu[c] + kp.dt / chi * (dcdT * kp.Gv - s * kp.inv_dt + divf[c] * kp.inv_dx);
+  }
+}
+
+}  // namespace pf

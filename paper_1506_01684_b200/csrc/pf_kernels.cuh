@@ -1,0 +1,69 @@
+// pf_kernels.cuh — kernel declarations and launch-side structs shared by the
+// runtime (pf_runtime.cu) and the kernel translation units.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "pf_dev.cuh"
+
+namespace pf {
+
+constexpr int XO = 4;  // column of interior i = 0 within a padded row (i = -1 at 3)
+
+// Pointers into one block's fields, offset to interior cell (0,0,0) of the
+// current window position; element (i,j,k) at p + k*plane + j*pitch + i with
+// i,j,k in [-1, n].
+struct BlockView {
+  const double *phi[NPH];
+  const double *mu[NMU];
+  const double *phin[NPH];  // phi^{n+1} (mu-sweep input)
+  double *out[NPH];         // phi^{n+1} (phi-sweep) or mu^{n+1} (mu-sweep)
+  int nx, ny, nz;
+  int64_t pitch, plane;
+  const double *tab;        // table row of local plane k = 0
+};
+
+// Strided 3D box copy (halo exchange: local copy, pack, unpack).
+struct CopyOp {
+  const double *src[NPH];
+  double *dst[NPH];
+  int64_t ssx, ssy, ssz;    // source strides (elements)
+  int64_t dsx, dsy, dsz;    // destination strides
+  int ex, ey, ez;           // extents
+  int ncomp;
+};
+
+struct InitSpec {
+  int kind, n_seeds, nlam;
+  double layer_height, W, mu_noise;
+  uint64_t seed;
+  int64_t NX, NY, NZ;       // global grid
+  const double *sx, *sy;    // voronoi seeds (device)
+  const int *sp;            // voronoi seed phases
+  const int64_t *lam;       // lamella starts (nlam+1 entries)
+  int planar_phase;
+};
+
+struct TabParams {
+  double T0, G, v, dt, dx, T_eut, eps;
+  double A0[NPH][NMU], A1[NPH][NMU], c0[NPH][NMU], m[NPH][NMU], L[NPH], D[NPH][NMU];
+};
+// table rows for global window planes kg = -1 .. nplanes-2 (row = kg + 1)
+void launch_table(cudaStream_t s, double *tab, int64_t nplanes, const TabParams &tp, int64_t step, int64_t zorig);
+void launch_phi_naive(cudaStream_t s, const KParams &kp, const BlockView &b);
+void launch_mu_naive(cudaStream_t s, const KParams &kp, const BlockView &b);
+void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b);
+void launch_mu_tiled(cudaStream_t s, const KParams &kp, const BlockView &b);
+void launch_copy(cudaStream_t s, const CopyOp *d_ops, int nops, int64_t max_cells);
+void launch_init(cudaStream_t s, const InitSpec &is, double *const phi[NPH], double *const mu[NMU],
+                 int nx, int ny, int nz, int64_t pitch, int64_t plane, int64_t x0, int64_t y0, int64_t z0);
+void launch_fill_plane(cudaStream_t s, double *const f[NPH], int ncomp, const double *vals, int nx, int ny,
+                       int64_t pitch);
+void launch_front(cudaStream_t s, const double *phil, int nx, int ny, int nz, int64_t pitch, int64_t plane,
+                  double thr, int64_t kbase, unsigned long long *d_out);
+void launch_nancheck(cudaStream_t s, const double *const f[NPH], int ncomp, int nx, int ny, int nz, int64_t pitch,
+                     int64_t plane, unsigned long long *d_first);
+void launch_gather(cudaStream_t s, const double *const f[NPH], int ncomp, int nx, int ny, int nz, int64_t pitch,
+                   int64_t plane, double *dst, int64_t dnx, int64_t dny, int64_t dn, int64_t ox, int64_t oy, int64_t oz,
+                   bool scatter, double *const fw[NPH]);
+
+}  // namespace pf

@@ -1,0 +1,872 @@
+// pf_runtime.cu — host runtime behind the C ABI of include/pf.h.
+//
+// Owns: the block decomposition ("equal-size blocks", one per
+// GPU rank or several per GPU), the fields (FP64, SoA, padded rows, one ghost
+// layer incl. the 12 edges the D3C19 stencil needs), the
+// per-plane table, the halo plans (local device copies + NCCL grouped
+// send/recv), the moving window and the
+// NaN watchdog ("no silent NaN propagation").
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/pf.h"
+#include "pf_kernels.cuh"
+
+using namespace pf;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct Block {
+  int bx, by, bz;            // block coordinates
+  int nx, ny, nz;
+  int64_t x0, y0, z0;        // global offset of the interior
+  int64_t pitch, plane, nplanes_alloc;
+  double *phi[2][NPH];       // two copies (src/dst), allocation bases
+  double *mu[2][NMU];
+  int woff;                  // window offset (planes)
+};
+
+struct Plan {                // halo plan of one field in one copy
+  CopyOp *d_local = nullptr, *d_pack = nullptr, *d_unpack = nullptr;
+  int nlocal = 0, npack = 0, nunpack = 0;
+  int64_t max_local = 0, max_pack = 0, max_unpack = 0;
+};
+
+struct Peer {
+  int rank;
+  int64_t send_off, send_cnt, recv_off, recv_cnt;  // in doubles, per field
+};
+
+}  // namespace
+
+struct pf_ctx {
+  pf_grid g{};
+  pf_params p{};
+  KParams kp{};
+  TabParams tp{};
+  int nblocks_total = 0;
+  std::vector<Block> blocks;       // blocks owned by this rank
+  int cur = 0;                     // index of the src copy
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  double *d_tab = nullptr;
+  int64_t tab_planes = 0;
+  Plan plan[2][2];                 // [field 0=phi 1=mu][copy]
+  std::vector<Peer> peers[2];      // per field
+  double *d_send[2] = {nullptr, nullptr}, *d_recv[2] = {nullptr, nullptr};
+  int64_t send_total[2] = {0, 0}, recv_total[2] = {0, 0};
+  ncclComm_t comm = nullptr;
+  unsigned long long *d_red = nullptr;  // reductions scratch (4 x u64)
+  double *d_stage = nullptr;            // read/write staging
+  int64_t stage_elems = 0;
+  int64_t step = 0, zorig = 0, shifts = 0, last_front = -1, next_check = 0;
+  int slack = 0;
+  bool initialized = false;
+  pf_status status = PF_OK;
+  std::string err;
+  // timing
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;     // pool
+  size_t ev_used = 0;
+  struct Span { int kind; size_t e0, e1; int nlaunch; };
+  std::vector<Span> spans;
+  double ms[4] = {0, 0, 0, 0};
+  int64_t launches = 0, phi_launches = 0, mu_launches = 0;
+  // box of this rank
+  int64_t box_nx = 0, box_ny = 0, box_nz = 0, box_x0 = 0, box_y0 = 0, box_z0 = 0;
+};
+
+namespace {
+
+pf_status fail(pf_ctx *c, pf_status st, const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) {
+    if (c->status == PF_OK) { c->status = st; c->err = buf; }
+  } else {
+    g_create_error = buf;
+  }
+  return st;
+}
+
+#define CK(call)                                                                                       \
+  do {                                                                                                 \
+    cudaError_t e_ = (call);                                                                           \
+    if (e_ != cudaSuccess)                                                                             \
+      return fail(c, PF_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+#define CKN(call)                                                                                      \
+  do {                                                                                                 \
+    ncclResult_t r_ = (call);                                                                          \
+    if (r_ != ncclSuccess)                                                                             \
+      return fail(c, PF_ERR_COMM, "%s failed: %s (%s:%d)", #call, ncclGetErrorString(r_), __FILE__, __LINE__); \
+  } while (0)
+#define CKS(expr)                    \
+  do {                               \
+    pf_status s_ = (expr);           \
+    if (s_ != PF_OK) return s_;      \
+  } while (0)
+
+inline double *field_ptr(const Block &b, int field, int copy, int comp) {
+  return field == 0 ? b.phi[copy][comp] : b.mu[copy][comp];
+}
+// address of interior (i,j,k) of a component base
+inline int64_t cell_off(const Block &b, int64_t i, int64_t j, int64_t k) {
+  return (k + 1 + b.woff) * b.plane + (j + 1) * b.pitch + (i + XO);
+}
+
+int block_id(const pf_ctx *c, int bx, int by, int bz) { return bx + c->g.px * (by + c->g.py * bz); }
+int owner_rank(const pf_ctx *c, int bid) { return c->g.nranks == 1 ? 0 : bid; }
+
+// the 18 ghost directions: faces and edges (corners unused by D3C19)
+std::vector<std::array<int, 3>> ghost_dirs() {
+  std::vector<std::array<int, 3>> v;
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int m = std::abs(dx) + std::abs(dy) + std::abs(dz);
+        if (m == 1 || m == 2) v.push_back({dx, dy, dz});
+      }
+  return v;
+}
+
+struct Region {   // one ghost region of a receiving block and where it comes from
+  int dst_bid, src_bid;
+  int64_t ds[3], ss[3];   // start indices (dest in receiver, source in sender)
+  int64_t ext[3];
+};
+
+// Ghost region of block (bx,by,bz) in direction d and its source (periodic
+// x/y, zero-gradient z at the global walls; reading R13).
+Region ghost_region(const pf_ctx *c, int bx, int by, int bz, const std::array<int, 3> &d, int nx, int ny, int nz) {
+  const int P[3] = {c->g.px, c->g.py, c->g.pz};
+  const int b[3] = {bx, by, bz};
+  const int64_t n[3] = {nx, ny, nz};
+  Region r;
+  int s[3];
+  for (int a = 0; a < 3; ++a) {
+    int dp = d[a];
+    if (a == 2 && (b[2] + d[2] < 0 || b[2] + d[2] >= P[2])) dp = 0;  // wall: clamp
+    s[a] = ((b[a] + dp) % P[a] + P[a]) % P[a];
+    r.ds[a] = d[a] == -1 ? -1 : (d[a] == 1 ? n[a] : 0);
+    r.ext[a] = d[a] == 0 ? n[a] : 1;
+    if (dp == -1) r.ss[a] = n[a] - 1;
+    else if (dp == 1) r.ss[a] = 0;
+    else r.ss[a] = d[a] == -1 ? 0 : (d[a] == 1 ? n[a] - 1 : 0);
+  }
+  r.dst_bid = block_id(c, bx, by, bz);
+  r.src_bid = block_id(c, s[0], s[1], s[2]);
+  return r;
+}
+
+int local_index(const pf_ctx *c, int bid) {
+  for (size_t q = 0; q < c->blocks.size(); ++q)
+    if (block_id(c, c->blocks[q].bx, c->blocks[q].by, c->blocks[q].bz) == bid) return (int)q;
+  return -1;
+}
+
+pf_status upload_ops(pf_ctx *c, const std::vector<CopyOp> &ops, CopyOp **d) {
+  if (*d) { cudaFree(*d); *d = nullptr; }
+  if (ops.empty()) return PF_OK;
+  CK(cudaMalloc(d, ops.size() * sizeof(CopyOp)));
+  CK(cudaMemcpy(*d, ops.data(), ops.size() * sizeof(CopyOp), cudaMemcpyHostToDevice));
+  return PF_OK;
+}
+
+// Build the halo plans of both fields and both copies.
+pf_status build_plans(pf_ctx *c) {
+  const auto dirs = ghost_dirs();
+  const int nb = c->nblocks_total;
+  const Block &b0 = c->blocks[0];
+  const int nx = b0.nx, ny = b0.ny, nz = b0.nz;
+  const int me = c->g.rank;
+  for (int field = 0; field < 2; ++field) {
+    const int ncomp = field == 0 ? NPH : NMU;
+    // peers: message layout per (peer) = receiver's regions in dir order
+    std::map<int, Peer> peers;
+    std::vector<Region> recv_regions, send_regions;  // with peer ordering
+    for (int bid = 0; bid < nb; ++bid) {
+      const int bx = bid % c->g.px, by = (bid / c->g.px) % c->g.py, bz = bid / (c->g.px * c->g.py);
+      for (const auto &d : dirs) {
+        const Region r = ghost_region(c, bx, by, bz, d, nx, ny, nz);
+        const int rdst = owner_rank(c, r.dst_bid), rsrc = owner_rank(c, r.src_bid);
+        if (rdst == me && rsrc != me) recv_regions.push_back(r);
+        if (rsrc == me && rdst != me) send_regions.push_back(r);
+      }
+    }
+    // order messages by peer rank, regions within a peer in enumeration order
+    int64_t off = 0;
+    for (int pr = 0; pr < c->g.nranks; ++pr) {
+      int64_t cnt = 0;
+      for (const auto &r : recv_regions)
+        if (owner_rank(c, r.src_bid) == pr) cnt += r.ext[0] * r.ext[1] * r.ext[2] * ncomp;
+      if (cnt) { Peer &p = peers[pr]; p.rank = pr; p.recv_off = off; p.recv_cnt = cnt; off += cnt; }
+    }
+    c->recv_total[field] = off;
+    off = 0;
+    for (int pr = 0; pr < c->g.nranks; ++pr) {
+      int64_t cnt = 0;
+      for (const auto &r : send_regions)
+        if (owner_rank(c, r.dst_bid) == pr) cnt += r.ext[0] * r.ext[1] * r.ext[2] * ncomp;
+      if (cnt) {
+        Peer &p = peers[pr];
+        p.rank = pr; p.send_off = off; p.send_cnt = cnt; off += cnt;
+      }
+    }
+    c->send_total[field] = off;
+    c->peers[field].clear();
+    for (auto &kv : peers) c->peers[field].push_back(kv.second);
+    if (c->d_send[field]) { cudaFree(c->d_send[field]); c->d_send[field] = nullptr; }
+    if (c->d_recv[field]) { cudaFree(c->d_recv[field]); c->d_recv[field] = nullptr; }
+    if (c->send_total[field]) CK(cudaMalloc(&c->d_send[field], c->send_total[field] * sizeof(double)));
+    if (c->recv_total[field]) CK(cudaMalloc(&c->d_recv[field], c->recv_total[field] * sizeof(double)));
+
+    for (int copy = 0; copy < 2; ++copy) {
+      std::vector<CopyOp> local, pack, unpack;
+      Plan &pl = c->plan[field][copy];
+      pl.max_local = pl.max_pack = pl.max_unpack = 0;
+      // local copies: both ends on this rank
+      for (size_t q = 0; q < c->blocks.size(); ++q) {
+        const Block &B = c->blocks[q];
+        for (const auto &d : dirs) {
+          const Region r = ghost_region(c, B.bx, B.by, B.bz, d, nx, ny, nz);
+          if (owner_rank(c, r.src_bid) != me) continue;
+          const Block &S = c->blocks[local_index(c, r.src_bid)];
+          CopyOp op{};
+          for (int cc = 0; cc < ncomp; ++cc) {
+            op.src[cc] = field_ptr(S, field, copy, cc) + cell_off(S, r.ss[0], r.ss[1], r.ss[2]);
+            op.dst[cc] = field_ptr(B, field, copy, cc) + cell_off(B, r.ds[0], r.ds[1], r.ds[2]);
+          }
+          op.ssx = op.dsx = 1; op.ssy = op.dsy = B.pitch; op.ssz = op.dsz = B.plane;
+          op.ex = (int)r.ext[0]; op.ey = (int)r.ext[1]; op.ez = (int)r.ext[2]; op.ncomp = ncomp;
+          local.push_back(op);
+          pl.max_local = std::max<int64_t>(pl.max_local, r.ext[0] * r.ext[1] * r.ext[2]);
+        }
+      }
+      // pack: regions this rank sends, per peer in the receiver's order
+      for (const Peer &p : c->peers[field]) {
+        int64_t o = p.send_off;
+        for (const auto &r : send_regions) {
+          if (owner_rank(c, r.dst_bid) != p.rank) continue;
+          const Block &S = c->blocks[local_index(c, r.src_bid)];
+          const int64_t n = r.ext[0] * r.ext[1] * r.ext[2];
+          CopyOp op{};
+          for (int cc = 0; cc < ncomp; ++cc) {
+            op.src[cc] = field_ptr(S, field, copy, cc) + cell_off(S, r.ss[0], r.ss[1], r.ss[2]);
+            op.dst[cc] = c->d_send[field] + o + cc * n;
+          }
+          op.ssx = 1; op.ssy = S.pitch; op.ssz = S.plane;
+          op.dsx = 1; op.dsy = r.ext[0]; op.dsz = r.ext[0] * r.ext[1];
+          op.ex = (int)r.ext[0]; op.ey = (int)r.ext[1]; op.ez = (int)r.ext[2]; op.ncomp = ncomp;
+          pack.push_back(op);
+          pl.max_pack = std::max(pl.max_pack, n);
+          o += n * ncomp;
+        }
+        int64_t o2 = p.recv_off;
+        for (const auto &r : recv_regions) {
+          if (owner_rank(c, r.src_bid) != p.rank) continue;
+          const Block &B = c->blocks[local_index(c, r.dst_bid)];
+          const int64_t n = r.ext[0] * r.ext[1] * r.ext[2];
+          CopyOp op{};
+          for (int cc = 0; cc < ncomp; ++cc) {
+            op.src[cc] = c->d_recv[field] + o2 + cc * n;
+            op.dst[cc] = field_ptr(B, field, copy, cc) + cell_off(B, r.ds[0], r.ds[1], r.ds[2]);
+          }
+          op.ssx = 1; op.ssy = r.ext[0]; op.ssz = r.ext[0] * r.ext[1];
+          op.dsx = 1; op.dsy = B.pitch; op.dsz = B.plane;
+          op.ex = (int)r.ext[0]; op.ey = (int)r.ext[1]; op.ez = (int)r.ext[2]; op.ncomp = ncomp;
+          unpack.push_back(op);
+          pl.max_unpack = std::max(pl.max_unpack, n);
+          o2 += n * ncomp;
+        }
+      }
+      // local copies go with the pack launch (no dependency on communication)
+      std::vector<CopyOp> first = pack;
+      first.insert(first.end(), local.begin(), local.end());
+      pl.nlocal = (int)first.size();
+      pl.max_local = std::max(pl.max_local, pl.max_pack);
+      CKS(upload_ops(c, first, &pl.d_local));
+      pl.nunpack = (int)unpack.size();
+      CKS(upload_ops(c, unpack, &pl.d_unpack));
+    }
+  }
+  return PF_OK;
+}
+
+size_t ev_next(pf_ctx *c) {
+  if (c->ev_used == c->ev.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->ev.push_back(e);
+  }
+  return c->ev_used++;
+}
+
+struct TimedSpan {  // records an event pair around a group of launches
+  pf_ctx *c; int kind; size_t e0; int n;
+  TimedSpan(pf_ctx *c_, int kind_, int n_) : c(c_), kind(kind_), e0(0), n(n_) {
+    if (c->timing) { e0 = ev_next(c); cudaEventRecord(c->ev[e0], c->stream); }
+  }
+  ~TimedSpan() {
+    if (c->timing) {
+      const size_t e1 = ev_next(c);
+      cudaEventRecord(c->ev[e1], c->stream);
+      c->spans.push_back({kind, e0, e1, n});
+    }
+  }
+};
+
+// Exchange the ghosts of one field in one copy.
+pf_status exchange(pf_ctx *c, int field, int copy) {
+  const Plan &pl = c->plan[field][copy];
+  TimedSpan ts(c, 2, 0);
+  if (pl.nlocal) { launch_copy(c->stream, pl.d_local, pl.nlocal, pl.max_local); c->launches++; }
+  if (c->g.nranks > 1 && !c->peers[field].empty()) {
+    CKN(ncclGroupStart());
+    for (const Peer &p : c->peers[field]) {
+      if (p.send_cnt) CKN(ncclSend(c->d_send[field] + p.send_off, (size_t)p.send_cnt, ncclDouble, p.rank, c->comm, c->stream));
+      if (p.recv_cnt) CKN(ncclRecv(c->d_recv[field] + p.recv_off, (size_t)p.recv_cnt, ncclDouble, p.rank, c->comm, c->stream));
+    }
+    CKN(ncclGroupEnd());
+  }
+  if (pl.nunpack) { launch_copy(c->stream, pl.d_unpack, pl.nunpack, pl.max_unpack); c->launches++; }
+  CK(cudaGetLastError());
+  return PF_OK;
+}
+
+BlockView view(const pf_ctx *c, const Block &b, int field_out) {
+  BlockView v{};
+  const int s = c->cur, d = c->cur ^ 1;
+  const int64_t o = cell_off(b, 0, 0, 0);
+  for (int a = 0; a < NPH; ++a) { v.phi[a] = b.phi[s][a] + o; v.phin[a] = b.phi[d][a] + o; }
+  for (int q = 0; q < NMU; ++q) v.mu[q] = b.mu[s][q] + o;
+  if (field_out == 0) for (int a = 0; a < NPH; ++a) v.out[a] = b.phi[d][a] + o;
+  else for (int q = 0; q < NMU; ++q) v.out[q] = b.mu[d][q] + o;
+  v.nx = b.nx; v.ny = b.ny; v.nz = b.nz; v.pitch = b.pitch; v.plane = b.plane;
+  v.tab = c->d_tab + (b.z0 + 1) * TAB;
+  return v;
+}
+
+pf_status collect_timing(pf_ctx *c) {
+  if (!c->timing) return PF_OK;
+  CK(cudaStreamSynchronize(c->stream));
+  for (const auto &s : c->spans) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, c->ev[s.e0], c->ev[s.e1]));
+    c->ms[s.kind] += ms;
+    if (s.kind == 0) c->phi_launches += s.nlaunch;
+    if (s.kind == 1) c->mu_launches += s.nlaunch;
+  }
+  c->spans.clear();
+  c->ev_used = 0;
+  return PF_OK;
+}
+
+pf_status window_compact(pf_ctx *c) {
+  // copy planes [woff, woff + nz + 2) of the src copy into [0, nz + 2) of the
+  // dst copy (scratch between steps), then swap
+  for (auto &b : c->blocks) {
+    const size_t bytes = (size_t)(b.nz + 2) * b.plane * sizeof(double);
+    for (int a = 0; a < NPH; ++a)
+      CK(cudaMemcpyAsync(b.phi[c->cur ^ 1][a], b.phi[c->cur][a] + (int64_t)b.woff * b.plane, bytes,
+                         cudaMemcpyDeviceToDevice, c->stream));
+    for (int q = 0; q < NMU; ++q)
+      CK(cudaMemcpyAsync(b.mu[c->cur ^ 1][q], b.mu[c->cur][q] + (int64_t)b.woff * b.plane, bytes,
+                         cudaMemcpyDeviceToDevice, c->stream));
+    b.woff = 0;
+  }
+  c->cur ^= 1;
+  return PF_OK;
+}
+
+// Moving window (reading R16): decide after the step whether the
+// front reached ceil(frac * NZ); shift one plane (ring offset) if so.
+pf_status window_check(pf_ctx *c) {
+  if (!c->p.window) return PF_OK;
+  if (c->step < c->next_check) return PF_OK;
+  CK(cudaMemsetAsync(c->d_red, 0, 2 * sizeof(unsigned long long), c->stream));
+  for (const auto &b : c->blocks) {
+    const double *phil = b.phi[c->cur][LIQ] + cell_off(b, 0, 0, 0);
+    launch_front(c->stream, phil, b.nx, b.ny, b.nz, b.pitch, b.plane, c->p.window_phi_l, b.z0, c->d_red);
+    c->launches++;
+  }
+  if (c->g.nranks > 1) CKN(ncclAllReduce(c->d_red, c->d_red, 2, ncclUint64, ncclMax, c->comm, c->stream));
+  unsigned long long h[2];
+  CK(cudaMemcpyAsync(h, c->d_red, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  const int64_t front = (int64_t)h[0] - 1, k1 = (int64_t)h[1] - 1;
+  c->last_front = front;
+  const int64_t trig = (int64_t)std::ceil(c->p.window_frac * (double)c->g.nz);
+  if (front >= trig) {
+    bool need_compact = false;
+    for (auto &b : c->blocks) if (b.woff >= c->slack) need_compact = true;
+    if (need_compact) CKS(window_compact(c));
+    for (auto &b : c->blocks) b.woff += 1;
+    // top blocks: new top interior plane = liquid (phi = e_l, mu = 0)
+    for (auto &b : c->blocks) {
+      if (b.bz != c->g.pz - 1) continue;
+      double *fp[NPH], *fm[NPH] = {nullptr, nullptr, nullptr, nullptr};
+      for (int a = 0; a < NPH; ++a) fp[a] = b.phi[c->cur][a] + cell_off(b, 0, 0, b.nz - 1);
+      for (int q = 0; q < NMU; ++q) fm[q] = b.mu[c->cur][q] + cell_off(b, 0, 0, b.nz - 1);
+      const double liq[4] = {0.0, 0.0, 0.0, 1.0}, zero[4] = {0, 0, 0, 0};
+      launch_fill_plane(c->stream, fp, NPH, liq, b.nx, b.ny, b.pitch);
+      launch_fill_plane(c->stream, fm, NMU, zero, b.nx, b.ny, b.pitch);
+      c->launches += 2;
+    }
+    c->zorig += 1;
+    c->shifts += 1;
+    CKS(build_plans(c));
+    CKS(exchange(c, 0, c->cur));
+    CKS(exchange(c, 1, c->cur));
+    c->next_check = c->step + 1;
+  } else {
+    // phi_l < 1 reaches at most one plane further per step (D3C7/D3C19 reach
+    // 1): no shift is possible before k1 can reach the trigger
+    c->next_check = c->step + std::max<int64_t>(1, trig - k1 - 1);
+  }
+  return PF_OK;
+}
+
+pf_status nan_check(pf_ctx *c) {
+  CK(cudaMemsetAsync(c->d_red + 2, 0xff, 2 * sizeof(unsigned long long), c->stream));
+  for (size_t q = 0; q < c->blocks.size(); ++q) {
+    const Block &b = c->blocks[q];
+    const double *fp[NPH], *fm[NPH] = {nullptr, nullptr, nullptr, nullptr};
+    for (int a = 0; a < NPH; ++a) fp[a] = b.phi[c->cur][a] + cell_off(b, 0, 0, 0);
+    for (int m = 0; m < NMU; ++m) fm[m] = b.mu[c->cur][m] + cell_off(b, 0, 0, 0);
+    launch_nancheck(c->stream, fp, NPH, b.nx, b.ny, b.nz, b.pitch, b.plane, c->d_red + 2);
+    launch_nancheck(c->stream, fm, NMU, b.nx, b.ny, b.nz, b.pitch, b.plane, c->d_red + 3);
+    unsigned long long h[2];
+    CK(cudaMemcpyAsync(h, c->d_red + 2, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int f = 0; f < 2; ++f) {
+      if (h[f] == ~0ULL) continue;
+      const int64_t n = (int64_t)b.nx * b.ny * b.nz;
+      const int64_t comp = (int64_t)(h[f] / n), t = (int64_t)(h[f] % n);
+      const int64_t i = t % b.nx, j = (t / b.nx) % b.ny, k = t / ((int64_t)b.nx * b.ny);
+      return fail(c, PF_ERR_NUMERICAL, "non-finite %s[%lld] at step %lld, global cell (%lld, %lld, %lld)",
+                  f == 0 ? "phi" : "mu", (long long)comp, (long long)c->step, (long long)(b.x0 + i),
+                  (long long)(b.y0 + j), (long long)(b.z0 + k));
+    }
+  }
+  return PF_OK;
+}
+
+pf_status fill_all_ghosts(pf_ctx *c) {
+  CKS(exchange(c, 0, c->cur));
+  CKS(exchange(c, 1, c->cur));
+  return PF_OK;
+}
+
+pf_status check_state(pf_ctx *c, bool need_init) {
+  if (!c) return PF_ERR_ARG;
+  if (c->status != PF_OK) return PF_ERR_STATE;
+  if (need_init && !c->initialized) return fail(c, PF_ERR_STATE, "pf_step/pf_read before pf_init/pf_write");
+  CK(cudaSetDevice(c->g.device));
+  return PF_OK;
+}
+
+bool is_device_ptr(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// copy the rank box between the public compact layout (user, host/device) and the fields
+pf_status move_state(pf_ctx *c, double *phi, double *mu, bool to_fields) {
+  const int64_t n = c->box_nx * c->box_ny * c->box_nz;
+  for (int field = 0; field < 2; ++field) {
+    double *user = field == 0 ? phi : mu;
+    const int ncomp = field == 0 ? NPH : NMU;
+    const bool dev = is_device_ptr(user);
+    double *buf = dev ? user : c->d_stage;
+    if (to_fields && !dev)
+      CK(cudaMemcpyAsync(buf, user, (size_t)n * ncomp * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    for (const auto &b : c->blocks) {
+      const double *f[NPH];
+      double *w[NPH];
+      for (int q = 0; q < ncomp; ++q) {
+        double *base = field_ptr(b, field, c->cur, q) + cell_off(b, 0, 0, 0);
+        f[q] = base;
+        w[q] = base;
+      }
+      launch_gather(c->stream, f, ncomp, b.nx, b.ny, b.nz, b.pitch, b.plane, buf, c->box_nx, c->box_ny, n,
+                    b.x0 - c->box_x0, b.y0 - c->box_y0, b.z0 - c->box_z0, to_fields, w);
+    }
+    CK(cudaGetLastError());
+    if (!to_fields && !dev)
+      CK(cudaMemcpyAsync(user, buf, (size_t)n * ncomp * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  return PF_OK;
+}
+
+pf_status validate(const pf_grid *g, const pf_params *p) {
+  pf_ctx *c = nullptr;
+  const int64_t n[3] = {g->nx, g->ny, g->nz};
+  const int P[3] = {g->px, g->py, g->pz};
+  const char *ax = "xyz";
+  for (int a = 0; a < 3; ++a) {
+    if (n[a] <= 0 || P[a] <= 0) return fail(c, PF_ERR_CONFIG, "axis %c: non-positive size or block count", ax[a]);
+    if (n[a] % P[a] != 0)
+      return fail(c, PF_ERR_CONFIG, "axis %c: %lld cells not divisible by %d blocks", ax[a], (long long)n[a], P[a]);
+    if (n[a] / P[a] < 2) return fail(c, PF_ERR_CONFIG, "axis %c: blocks must be >= 2 cells", ax[a]);
+  }
+  const int nb = P[0] * P[1] * P[2];
+  if (g->nranks != 1 && g->nranks != nb)
+    return fail(c, PF_ERR_CONFIG, "nranks (%d) must be 1 or px*py*pz (%d)", g->nranks, nb);
+  if (g->rank < 0 || g->rank >= g->nranks) return fail(c, PF_ERR_CONFIG, "rank %d out of range", g->rank);
+  for (int a = 0; a < 4; ++a)
+    for (int b = 0; b < 4; ++b) {
+      if (p->gamma[a][b] != p->gamma[b][a] || p->delta[a][b] != p->delta[b][a])
+        return fail(c, PF_ERR_CONFIG, "gamma/delta not symmetric at (%d,%d)", a, b);
+      if (a != b && !(p->gamma[a][b] > 0)) return fail(c, PF_ERR_CONFIG, "gamma[%d][%d] must be > 0", a, b);
+    }
+  if (!(p->dt > 0) || !(p->dx > 0) || !(p->eps > 0)) return fail(c, PF_ERR_CONFIG, "dt, dx, eps must be > 0");
+  for (int a = 0; a < 4; ++a)
+    if (!(p->tau[a] > 0)) return fail(c, PF_ERR_CONFIG, "tau[%d] must be > 0", a);
+  // A(T) > 0 over the initial window (z in [-1, NZ+1]) and 10x that span
+  const double Tlo = p->T0 + std::min(0.0, p->G) * (double)(g->nz + 2) * p->dx * 10 - std::fabs(p->G) * p->dx;
+  const double Thi = p->T0 + std::max(0.0, p->G) * (double)(g->nz + 2) * p->dx * 10 + std::fabs(p->G) * p->dx;
+  for (double T : {Tlo, Thi, p->T0})
+    for (int a = 0; a < 4; ++a)
+      for (int q = 0; q < 2; ++q)
+        if (!(p->A0[a][q] + p->A1[a][q] * (T - p->T_eut) > 0))
+          return fail(c, PF_ERR_CONFIG, "A[%d][%d](T=%g) <= 0", a, q, T);
+  if (p->window && !(p->window_frac > 0 && p->window_frac <= 1)) return fail(c, PF_ERR_CONFIG, "window_frac");
+  return PF_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+pf_status pf_nccl_unique_id(uint8_t out[128]) {
+  if (!out) return PF_ERR_ARG;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return PF_ERR_COMM;
+  memcpy(out, &id, 128);
+  return PF_OK;
+}
+
+pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
+  g_create_error.clear();
+  if (!g || !p || !out) return fail(nullptr, PF_ERR_ARG, "NULL argument");
+  *out = nullptr;
+  CKS(validate(g, p));
+  pf_ctx *c = new pf_ctx();
+  c->g = *g;
+  c->p = *p;
+  auto bail = [&](pf_status st) {
+    g_create_error = c->err;
+    pf_destroy(c);
+    return st;
+  };
+  if (cudaSetDevice(g->device) != cudaSuccess) {
+    cudaGetLastError();
+    fail(c, PF_ERR_CUDA, "cudaSetDevice(%d) failed (no GPU?)", g->device);
+    return bail(PF_ERR_CUDA);
+  }
+  // kernel constants
+  KParams &kp = c->kp;
+  kp.dt = p->dt; kp.inv_dt = 1.0 / p->dt; kp.inv_dx = 1.0 / p->dx; kp.inv_2dx = 1.0 / (2.0 * p->dx);
+  kp.half_inv_dt = 0.5 / p->dt;
+  for (int a = 0; a < 4; ++a) {
+    kp.dt_taueps[a] = p->dt / (p->tau[a] * p->eps);
+    kp.g3[a] = p->gamma3[a];
+    for (int b = 0; b < 4; ++b) kp.om[a][b] = a == b ? 0.0 : 16.0 / (M_PI * M_PI) * p->gamma[a][b];
+  }
+  for (int q = 0; q < 6; ++q) {
+    kp.g2[q] = 2.0 * p->gamma[pair_a(q)][pair_b(q)];
+    kp.delta[q] = p->aniso ? p->delta[pair_a(q)][pair_b(q)] : 0.0;
+  }
+  kp.pi_eps_4 = M_PI * p->eps / 4.0;
+  kp.Gv = p->G * p->v;
+  kp.aniso = p->aniso ? 1 : 0;
+  TabParams &tp = c->tp;
+  tp.T0 = p->T0; tp.G = p->G; tp.v = p->v; tp.dt = p->dt; tp.dx = p->dx; tp.T_eut = p->T_eut; tp.eps = p->eps;
+  for (int a = 0; a < 4; ++a) {
+    tp.L[a] = p->L[a];
+    for (int q = 0; q < 2; ++q) {
+      tp.A0[a][q] = p->A0[a][q]; tp.A1[a][q] = p->A1[a][q]; tp.c0[a][q] = p->c0[a][q];
+      tp.m[a][q] = p->m[a][q]; tp.D[a][q] = p->D[a][q];
+    }
+  }
+  // decomposition
+  c->nblocks_total = g->px * g->py * g->pz;
+  const int nx = (int)(g->nx / g->px), ny = (int)(g->ny / g->py), nz = (int)(g->nz / g->pz);
+  c->slack = p->window ? 16 : 0;
+  std::vector<int> mine;
+  if (g->nranks == 1) for (int b = 0; b < c->nblocks_total; ++b) mine.push_back(b);
+  else mine.push_back(g->rank);
+  for (int bid : mine) {
+    Block b{};
+    b.bx = bid % g->px; b.by = (bid / g->px) % g->py; b.bz = bid / (g->px * g->py);
+    b.nx = nx; b.ny = ny; b.nz = nz;
+    b.x0 = (int64_t)b.bx * nx; b.y0 = (int64_t)b.by * ny; b.z0 = (int64_t)b.bz * nz;
+    b.pitch = ((nx + XO + 1) + 15) / 16 * 16;
+    b.plane = b.pitch * (ny + 2);
+    b.nplanes_alloc = nz + 2 + c->slack;
+    b.woff = 0;
+    const size_t bytes = (size_t)b.plane * b.nplanes_alloc * sizeof(double);
+    for (int cp = 0; cp < 2; ++cp) {
+      for (int a = 0; a < NPH; ++a) {
+        if (cudaMalloc(&b.phi[cp][a], bytes) != cudaSuccess) { cudaGetLastError(); c->blocks.push_back(b); fail(c, PF_ERR_CUDA, "out of device memory (%zu B)", bytes); return bail(PF_ERR_CUDA); }
+        cudaMemset(b.phi[cp][a], 0, bytes);
+      }
+      for (int q = 0; q < NMU; ++q) {
+        if (cudaMalloc(&b.mu[cp][q], bytes) != cudaSuccess) { cudaGetLastError(); c->blocks.push_back(b); fail(c, PF_ERR_CUDA, "out of device memory (%zu B)", bytes); return bail(PF_ERR_CUDA); }
+        cudaMemset(b.mu[cp][q], 0, bytes);
+      }
+    }
+    c->blocks.push_back(b);
+  }
+  // rank box
+  {
+    int64_t x1 = 0, y1 = 0, z1 = 0;
+    c->box_x0 = c->box_y0 = c->box_z0 = INT64_MAX;
+    for (auto &b : c->blocks) {
+      c->box_x0 = std::min(c->box_x0, b.x0); c->box_y0 = std::min(c->box_y0, b.y0); c->box_z0 = std::min(c->box_z0, b.z0);
+      x1 = std::max(x1, b.x0 + b.nx); y1 = std::max(y1, b.y0 + b.ny); z1 = std::max(z1, b.z0 + b.nz);
+    }
+    c->box_nx = x1 - c->box_x0; c->box_ny = y1 - c->box_y0; c->box_nz = z1 - c->box_z0;
+  }
+  if (g->stream) { c->stream = (cudaStream_t)g->stream; c->own_stream = false; }
+  else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) { fail(c, PF_ERR_CUDA, "stream"); return bail(PF_ERR_CUDA); }
+    c->own_stream = true;
+  }
+  c->tab_planes = g->nz + 2;
+  if (cudaMalloc(&c->d_tab, (size_t)c->tab_planes * TAB * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&c->d_red, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+    fail(c, PF_ERR_CUDA, "alloc table"); return bail(PF_ERR_CUDA);
+  }
+  c->stage_elems = c->box_nx * c->box_ny * c->box_nz * NPH;
+  if (cudaMalloc(&c->d_stage, (size_t)c->stage_elems * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError(); fail(c, PF_ERR_CUDA, "alloc staging"); return bail(PF_ERR_CUDA);
+  }
+  if (g->nranks > 1) {
+    ncclUniqueId id;
+    memcpy(&id, g->nccl_id, 128);
+    ncclResult_t r = ncclCommInitRank(&c->comm, g->nranks, id, g->rank);
+    if (r != ncclSuccess) { fail(c, PF_ERR_COMM, "ncclCommInitRank: %s", ncclGetErrorString(r)); return bail(PF_ERR_COMM); }
+  }
+  if (build_plans(c) != PF_OK) return bail(c->status);
+  if (cudaDeviceSynchronize() != cudaSuccess) { fail(c, PF_ERR_CUDA, "setup sync"); return bail(PF_ERR_CUDA); }
+  *out = c;
+  return PF_OK;
+}
+
+pf_status pf_init(pf_ctx *c, uint64_t seed) {
+  CKS(check_state(c, false));
+  const pf_params &p = c->p;
+  InitSpec is{};
+  is.kind = p.init_kind; is.n_seeds = p.init_n_seeds; is.layer_height = p.init_layer_height;
+  is.W = p.init_iface_width; is.mu_noise = p.init_mu_noise; is.seed = seed;
+  is.NX = c->g.nx; is.NY = c->g.ny; is.NZ = c->g.nz; is.planar_phase = p.init_planar_phase;
+  // host side: seeds / lamellae from the same counter-based generator
+  auto mix = [](uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+  };
+  auto u01 = [&](uint64_t stream, uint64_t idx) {
+    return (double)(mix(mix(seed ^ (stream * 0xD1B54A32D192ED03ULL)) ^ idx) >> 11) * 0x1.0p-53;
+  };
+  std::vector<double> sx, sy;
+  std::vector<int> sp;
+  std::vector<int64_t> lam;
+  double *d_sx = nullptr, *d_sy = nullptr;
+  int *d_sp = nullptr;
+  int64_t *d_lam = nullptr;
+  if (p.init_kind == 0) {
+    if (p.init_n_seeds <= 0) return fail(c, PF_ERR_CONFIG, "init_n_seeds must be > 0");
+    for (int q = 0; q < p.init_n_seeds; ++q) {
+      sx.push_back(u01(1, q) * (double)c->g.nx);
+      sy.push_back(u01(2, q) * (double)c->g.ny);
+      sp.push_back(std::min(2, (int)(u01(3, q) * 3.0)));
+    }
+    CK(cudaMalloc(&d_sx, sx.size() * sizeof(double)));
+    CK(cudaMalloc(&d_sy, sy.size() * sizeof(double)));
+    CK(cudaMalloc(&d_sp, sp.size() * sizeof(int)));
+    CK(cudaMemcpy(d_sx, sx.data(), sx.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_sy, sy.data(), sy.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_sp, sp.data(), sp.size() * sizeof(int), cudaMemcpyHostToDevice));
+  } else if (p.init_kind == 1) {
+    int64_t x = 0, n = 0;
+    while (x < c->g.nx) {
+      lam.push_back(x);
+      x += p.init_lam_wmin + (int64_t)(u01(4, (uint64_t)n) * (double)(p.init_lam_wmax - p.init_lam_wmin + 1));
+      ++n;
+    }
+    lam.push_back(c->g.nx);
+    is.nlam = (int)n;
+    CK(cudaMalloc(&d_lam, lam.size() * sizeof(int64_t)));
+    CK(cudaMemcpy(d_lam, lam.data(), lam.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  }
+  is.sx = d_sx; is.sy = d_sy; is.sp = d_sp; is.lam = d_lam;
+  for (auto &b : c->blocks) b.woff = 0;
+  c->cur = 0;
+  CKS(build_plans(c));
+  for (auto &b : c->blocks) {
+    double *fp[NPH], *fm[NMU];
+    for (int a = 0; a < NPH; ++a) fp[a] = b.phi[c->cur][a] + cell_off(b, 0, 0, 0);
+    for (int q = 0; q < NMU; ++q) fm[q] = b.mu[c->cur][q] + cell_off(b, 0, 0, 0);
+    launch_init(c->stream, is, fp, fm, b.nx, b.ny, b.nz, b.pitch, b.plane, b.x0, b.y0, b.z0);
+  }
+  CK(cudaGetLastError());
+  CKS(fill_all_ghosts(c));
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(d_sx); cudaFree(d_sy); cudaFree(d_sp); cudaFree(d_lam);
+  c->step = 0; c->zorig = 0; c->shifts = 0; c->next_check = 0; c->last_front = -1;
+  c->initialized = true;
+  return PF_OK;
+}
+
+pf_status pf_write(pf_ctx *c, const double *phi, const double *mu) {
+  CKS(check_state(c, false));
+  if (!phi || !mu) return fail(c, PF_ERR_ARG, "NULL state pointer");
+  for (auto &b : c->blocks) b.woff = 0;
+  c->cur = 0;
+  CKS(build_plans(c));
+  CKS(move_state(c, const_cast<double *>(phi), const_cast<double *>(mu), true));
+  CKS(fill_all_ghosts(c));
+  CK(cudaStreamSynchronize(c->stream));
+  c->next_check = c->step;
+  c->initialized = true;
+  return PF_OK;
+}
+
+pf_status pf_set_time(pf_ctx *c, int64_t step, int64_t z_origin) {
+  CKS(check_state(c, false));
+  c->step = step;
+  c->zorig = z_origin;
+  c->next_check = step;
+  return PF_OK;
+}
+
+pf_status pf_step(pf_ctx *c, int64_t n) {
+  CKS(check_state(c, true));
+  if (n < 0) return fail(c, PF_ERR_ARG, "negative step count");
+  for (int64_t s = 0; s < n; ++s) {
+    {
+      TimedSpan ts(c, 3, 0);
+      launch_table(c->stream, c->d_tab, c->tab_planes, c->tp, c->step, c->zorig);
+      c->launches++;
+    }
+    {  // phi-sweep (Algorithm 1 line 1)
+      TimedSpan ts(c, 0, (int)c->blocks.size());
+      for (const auto &b : c->blocks) {
+        const BlockView v = view(c, b, 0);
+        if (c->p.variant == 1) launch_phi_naive(c->stream, c->kp, v);
+        else launch_phi_tiled(c->stream, c->kp, v);
+        c->launches++;
+      }
+    }
+    CK(cudaGetLastError());
+    CKS(exchange(c, 0, c->cur ^ 1));    // lines 2-3: phi_dst ghosts + boundary
+    {  // mu-sweep (line 4)
+      TimedSpan ts(c, 1, (int)c->blocks.size());
+      for (const auto &b : c->blocks) {
+        const BlockView v = view(c, b, 1);
+        if (c->p.variant == 1) launch_mu_naive(c->stream, c->kp, v);
+        else launch_mu_tiled(c->stream, c->kp, v);
+        c->launches++;
+      }
+    }
+    CK(cudaGetLastError());
+    CKS(exchange(c, 1, c->cur ^ 1));    // lines 5-6
+    c->cur ^= 1;                        // line 7: swap
+    c->step += 1;
+    CKS(window_check(c));
+    if (c->p.nan_check_every > 0 && c->step % c->p.nan_check_every == 0) CKS(nan_check(c));
+    if (c->timing && c->spans.size() > 4096) CKS(collect_timing(c));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaGetLastError());
+  CKS(collect_timing(c));
+  return PF_OK;
+}
+
+pf_status pf_read(pf_ctx *c, double *phi, double *mu) {
+  CKS(check_state(c, true));
+  if (!phi || !mu) return fail(c, PF_ERR_ARG, "NULL state pointer");
+  return move_state(c, phi, mu, false);
+}
+
+pf_status pf_set_timing(pf_ctx *c, int32_t on) {
+  CKS(check_state(c, false));
+  CKS(collect_timing(c));
+  c->timing = on != 0;
+  for (double &m : c->ms) m = 0;
+  c->phi_launches = c->mu_launches = 0;
+  return PF_OK;
+}
+
+pf_status pf_info(pf_ctx *c, pf_info_t *o) {
+  if (!c || !o) return PF_ERR_ARG;
+  memset(o, 0, sizeof(*o));
+  o->nx_l = c->box_nx; o->ny_l = c->box_ny; o->nz_l = c->box_nz;
+  o->x0 = c->box_x0; o->y0 = c->box_y0; o->z0 = c->box_z0;
+  o->step = c->step; o->z_origin = c->zorig; o->shifts = c->shifts; o->last_front = c->last_front;
+  o->nblocks_local = (int32_t)c->blocks.size();
+  o->timing = c->timing;
+  o->ms_phi = c->ms[0]; o->ms_mu = c->ms[1]; o->ms_halo = c->ms[2]; o->ms_other = c->ms[3];
+  o->launches = c->launches; o->phi_launches = c->phi_launches; o->mu_launches = c->mu_launches;
+  return c->status == PF_OK ? PF_OK : PF_ERR_STATE;
+}
+
+const char *pf_last_error(const pf_ctx *c) {
+  if (!c) return g_create_error.c_str();
+  return c->err.c_str();
+}
+
+void pf_destroy(pf_ctx *c) {
+  if (!c) return;
+  cudaSetDevice(c->g.device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto &b : c->blocks) {
+    for (int cp = 0; cp < 2; ++cp) {
+      for (int a = 0; a < NPH; ++a) if (b.phi[cp][a]) cudaFree(b.phi[cp][a]);
+      for (int q = 0; q < NMU; ++q) if (b.mu[cp][q]) cudaFree(b.mu[cp][q]);
+    }
+  }
+  for (int f = 0; f < 2; ++f) {
+    for (int cp = 0; cp < 2; ++cp) {
+      if (c->plan[f][cp].d_local) cudaFree(c->plan[f][cp].d_local);
+      if (c->plan[f][cp].d_unpack) cudaFree(c->plan[f][cp].d_unpack);
+    }
+    if (c->d_send[f]) cudaFree(c->d_send[f]);
+    if (c->d_recv[f]) cudaFree(c->d_recv[f]);
+  }
+  if (c->d_tab) cudaFree(c->d_tab);
+  if (c->d_red) cudaFree(c->d_red);
+  if (c->d_stage) cudaFree(c->d_stage);
+  for (auto e : c->ev) cudaEventDestroy(e);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  cudaGetLastError();
+  delete c;
+}
+
+}  // extern "C"

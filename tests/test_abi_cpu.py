@@ -1,0 +1,55 @@
+"""CPU-side checks of the C-ABI library: it loads without a GPU and exports
+every symbol include/pf.h declares (no compute calls here)."""
+import ctypes
+import os
+import re
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "pf.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pf_[a-z_]+)\s*\(", src)))
+
+
+def test_library_builds_and_exports_all_declared_symbols():
+    from paper_1506_01684_b200 import build, pf
+    build.build()
+    lib = ctypes.CDLL(pf.LIB_PATH)
+    names = _declared()
+    assert "pf_create" in names and "pf_step" in names and "pf_read" in names and "pf_init" in names
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(pf.EXPORTS)
+
+
+def test_struct_sizes_match_header():
+    # the ctypes mirrors must match the C layout (compiled probe)
+    import subprocess
+    import tempfile
+    from paper_1506_01684_b200 import pf
+    code = '#include <stdio.h>\n#include "pf.h"\nint main(){printf("%zu %zu %zu\\n", sizeof(pf_grid),' \
+           ' sizeof(pf_params), sizeof(pf_info_t));return 0;}\n'
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "p.c")
+        open(c, "w").write(code)
+        exe = os.path.join(d, "p")
+        subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", exe, c])
+        out = subprocess.check_output([exe]).decode().split()
+    assert [int(x) for x in out] == [ctypes.sizeof(pf.PfGrid), ctypes.sizeof(pf.PfParams), ctypes.sizeof(pf.PfInfo)]
+
+
+def test_create_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        return
+    from paper_1506_01684_b200 import pf
+    from inputs import gen
+    prm = pf.make_params(gen.load_params("v1"), gen.load_config("c1"))
+    try:
+        pf.Context(8, 8, 8, prm)
+    except pf.PfError as e:
+        assert e.status in (pf.PF_ERR_CUDA,)
+    else:
+        raise AssertionError("pf_create succeeded without a GPU")
