@@ -8,8 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpf.so")
-SOURCES = ["pf_runtime.cu", "pf_kernels.cu", "pf_tiled.cu"]
-HEADERS = ["pf_dev.cuh", "pf_kernels.cuh"]
+SOURCES = ["pf_runtime.cu", "pf_kernels.cu", "pf_phi.cu", "pf_mu.cu"]
+HEADERS = ["pf_dev.cuh", "pf_kernels.cuh", "pf_tile.cuh"]
 
 
 def _nccl_dirs():

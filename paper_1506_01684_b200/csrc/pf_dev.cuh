@@ -48,8 +48,11 @@ enum {
   T_MC = 35,      // + a*2 + c   D / (2A)
   T_B = 43,       // + a         L (T - T_eut) / T_eut
   T_MCHAT = 47,   // + a*2+c     m (as given; constant, kept for locality)
-  TAB = 56
+  T_DI2A = 55,    // + a*2+c     1/(2A^l) - 1/(2A^a), solids a < 3
+  T_DCHAT = 61,   // + a*2+c     chat^l - chat^a,     solids a < 3
+  TAB = 68        // multiple of 4 doubles (32 B): rows stay aligned
 };
+static_assert(TAB % 4 == 0, "table row alignment");
 
 #define RN_ADD __dadd_rn
 #define RN_SUB __dsub_rn
@@ -137,12 +140,27 @@ __device__ __forceinline__ double cgrad(const KParams &kp, double lo, double hi)
 }
 
 // Cell part of the phi update (oracle O4.1-4.11) given the cell value, its
-// chemical potential, centre gradients, the 6 face fluxes (jm: lower faces,
-// jp: upper faces, per direction) and the plane's table row.
+// chemical potential, centre gradients, the face-flux divergence sum_d (j^+ -
+// j^-) (before the 1/dx factor) and the plane's table row.
+__device__ __forceinline__ void phi_cell_update_div(const KParams &kp, const double *__restrict__ tab,
+                                                    const double ph[NPH], const double mu[NMU],
+                                                    const double gc[NPH][3], const double dsum[NPH],
+                                                    double out[NPH]);
+
 __device__ __forceinline__ void phi_cell_update(const KParams &kp, const double *__restrict__ tab,
                                                 const double ph[NPH], const double mu[NMU],
                                                 const double gc[NPH][3], const double jm[3][NPH],
                                                 const double jp[3][NPH], double out[NPH]) {
+  double dsum[NPH];
+#pragma unroll
+  for (int a = 0; a < NPH; ++a) dsum[a] = (jp[0][a] - jm[0][a]) + (jp[1][a] - jm[1][a]) + (jp[2][a] - jm[2][a]);
+  phi_cell_update_div(kp, tab, ph, mu, gc, dsum, out);
+}
+
+__device__ __forceinline__ void phi_cell_update_div(const KParams &kp, const double *__restrict__ tab,
+                                                    const double ph[NPH], const double mu[NMU],
+                                                    const double gc[NPH][3], const double dsum[NPH],
+                                                    double out[NPH]) {
   // d a / d phi_a = sum_{b != a} g_ab(q_ab) . grad phi_b   (O4.2-4)
   double dad[NPH] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -178,7 +196,7 @@ __device__ __forceinline__ void phi_cell_update(const KParams &kp, const double 
 #pragma unroll
   for (int a = 0; a < NPH; ++a) {
     // O4.6 divergence of the face fluxes
-    const double div = ((jp[0][a] - jm[0][a]) + (jp[1][a] - jm[1][a]) + (jp[2][a] - jm[2][a])) * kp.inv_dx;
+    const double div = dsum[a] * kp.inv_dx;
     // O4.7 multi-obstacle derivative
     double om = 0.0;
 #pragma unroll
@@ -232,6 +250,19 @@ struct MuQ {
   double mu[NMU];
 };
 
+// c^l - c^a = mu (1/(2A^l) - 1/(2A^a)) + (chat^l - chat^a) at the plane's T
+// (per-plane differences from the table; pinned).
+__device__ __forceinline__ double dcl_of(const double *__restrict__ tab, int a, int c, double mu) {
+  return RN_FMA(mu, tab[T_DI2A + a * 2 + c], tab[T_DCHAT + a * 2 + c]);
+}
+// mobility sum_a phi^n_a D/(2A) (pinned)
+__device__ __forceinline__ double mob_of(const double *__restrict__ tab, int c, const double po[NPH]) {
+  double M = RN_MUL(po[0], tab[T_MC + 0 * 2 + c]);
+  M = RN_FMA(po[1], tab[T_MC + 1 * 2 + c], M);
+  M = RN_FMA(po[2], tab[T_MC + 2 * 2 + c], M);
+  return RN_FMA(po[3], tab[T_MC + 3 * 2 + c], M);
+}
+
 __device__ __forceinline__ void mu_cell_q(const double *__restrict__ tab, const double po[NPH],
                                           const double pn[NPH], const double mu[NMU], MuQ &q) {
 #pragma unroll
@@ -239,57 +270,81 @@ __device__ __forceinline__ void mu_cell_q(const double *__restrict__ tab, const 
 #pragma unroll
   for (int c = 0; c < NMU; ++c) {
     q.mu[c] = mu[c];
-    double M = RN_MUL(po[0], tab[T_MC + 0 * 2 + c]);
-    M = RN_FMA(po[1], tab[T_MC + 1 * 2 + c], M);
-    M = RN_FMA(po[2], tab[T_MC + 2 * 2 + c], M);
-    M = RN_FMA(po[3], tab[T_MC + 3 * 2 + c], M);
-    q.M[c] = M;
-    // c^a = mu * inv2A + chat;  c^l - c^a
-    const double cl = RN_FMA(mu[c], tab[T_INV2A + LIQ * 2 + c], tab[T_CHAT + LIQ * 2 + c]);
+    q.M[c] = mob_of(tab, c, po);
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
-      q.dcl[a][c] = RN_SUB(cl, RN_FMA(mu[c], tab[T_INV2A + a * 2 + c], tab[T_CHAT + a * 2 + c]));
+    for (int a = 0; a < 3; ++a) q.dcl[a][c] = dcl_of(tab, a, c, mu[c]);
   }
 }
 
 // (M grad mu - J_at)_c at the face (lo, hi = lo + e_d) — oracle mu_face.
-// Pinned rounding; guards are exact-zero tests (reading R10).
-__device__ __forceinline__ void mu_face(const KParams &kp, const MuQ &lo, const MuQ &hi, int d, double out[NMU]) {
+// One pinned implementation for every operand source: QL / QH are accessors
+// (registers: MuQAcc; shared-memory tiles: see pf_mu.cu) with
+//   pn(a), dp(a) (a < 3), gt(a, e) (centre gradient of phi^{n+1}, e != d),
+//   M(c), mu(c), dcl(a, c).
+// Guards are exact-zero tests (reading R10).  The anti-trapping weight
+//   (pi eps/4) phi_a h_l / sqrt(phi_a phi_l) * dphi_a/dt * (n_a . n_l) * n_a,d
+// is evaluated as (pi eps/4) pb_a h_l pd (g_a . g_l) g_a,d / sqrt(pal |g_l|^2 |g_a|^4)
+// — one FP64 rsqrt per solid instead of three (algebraically identical; a
+// guarded fallback keeps it finite when the product leaves the normal range).
+template <class QL, class QH>
+__device__ __forceinline__ void mu_face_t(const KParams &kp, const QL &lo, const QH &hi, int d, double out[NMU]) {
 #pragma unroll
   for (int c = 0; c < NMU; ++c)
-    out[c] = RN_MUL(RN_MUL(RN_MUL(0.5, RN_ADD(lo.M[c], hi.M[c])), RN_SUB(hi.mu[c], lo.mu[c])), kp.inv_dx);
-  double pb[NPH], gf[NPH][3];
+    out[c] = RN_MUL(RN_MUL(RN_MUL(0.5, RN_ADD(lo.M(c), hi.M(c))), RN_SUB(hi.mu(c), lo.mu(c))), kp.inv_dx);
+  const double pbl = RN_MUL(0.5, RN_ADD(lo.pn(LIQ), hi.pn(LIQ)));
+  double gfl[3];
 #pragma unroll
-  for (int a = 0; a < NPH; ++a) {
-    pb[a] = RN_MUL(0.5, RN_ADD(lo.pn[a], hi.pn[a]));
+  for (int e = 0; e < 3; ++e)
+    gfl[e] = (e == d) ? RN_MUL(RN_SUB(hi.pn(LIQ), lo.pn(LIQ)), kp.inv_dx)
+                      : RN_MUL(0.5, RN_ADD(lo.gt(LIQ, e), hi.gt(LIQ, e)));
+  const double gl2 = RN_FMA(gfl[2], gfl[2], RN_FMA(gfl[1], gfl[1], RN_MUL(gfl[0], gfl[0])));
+  if (pbl == 0.0 || gl2 == 0.0) return;     // no liquid / flat liquid: J = 0
+  double pb[3];
 #pragma unroll
-    for (int e = 0; e < 3; ++e)
-      gf[a][e] = (e == d) ? RN_MUL(RN_SUB(hi.pn[a], lo.pn[a]), kp.inv_dx)
-                          : RN_MUL(0.5, RN_ADD(lo.gn[a][e], hi.gn[a][e]));
-  }
-  const double gl2 = RN_FMA(gf[LIQ][2], gf[LIQ][2], RN_FMA(gf[LIQ][1], gf[LIQ][1], RN_MUL(gf[LIQ][0], gf[LIQ][0])));
-  if (pb[LIQ] == 0.0 || gl2 == 0.0) return;     // no liquid / flat liquid: J = 0
-  const double S = RN_FMA(pb[3], pb[3], RN_FMA(pb[2], pb[2], RN_FMA(pb[1], pb[1], RN_MUL(pb[0], pb[0]))));
-  const double hl = __ddiv_rn(RN_MUL(pb[LIQ], pb[LIQ]), S);
-  const double rl = rsqrt(gl2);
+  for (int a = 0; a < 3; ++a) pb[a] = RN_MUL(0.5, RN_ADD(lo.pn(a), hi.pn(a)));
+  const double S = RN_FMA(pbl, pbl, RN_FMA(pb[2], pb[2], RN_FMA(pb[1], pb[1], RN_MUL(pb[0], pb[0]))));
+  const double hl = RN_MUL(RN_MUL(pbl, pbl), __drcp_rn(S));
   double J0 = 0.0, J1 = 0.0;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    const double pal = RN_MUL(pb[a], pb[LIQ]);
-    const double ga2 = RN_FMA(gf[a][2], gf[a][2], RN_FMA(gf[a][1], gf[a][1], RN_MUL(gf[a][0], gf[a][0])));
-    const double pd = RN_MUL(RN_ADD(lo.dp[a], hi.dp[a]), kp.half_inv_dt);
+    const double pal = RN_MUL(pb[a], pbl);
+    const double pd = RN_MUL(RN_ADD(lo.dp(a), hi.dp(a)), kp.half_inv_dt);
+    double gfa[3];
+#pragma unroll
+    for (int e = 0; e < 3; ++e)
+      gfa[e] = (e == d) ? RN_MUL(RN_SUB(hi.pn(a), lo.pn(a)), kp.inv_dx)
+                        : RN_MUL(0.5, RN_ADD(lo.gt(a, e), hi.gt(a, e)));
+    const double ga2 = RN_FMA(gfa[2], gfa[2], RN_FMA(gfa[1], gfa[1], RN_MUL(gfa[0], gfa[0])));
     if (pal == 0.0 || ga2 == 0.0 || pd == 0.0) continue;
-    const double ra = rsqrt(ga2);
-    const double dot = RN_FMA(gf[a][2], gf[LIQ][2], RN_FMA(gf[a][1], gf[LIQ][1], RN_MUL(gf[a][0], gf[LIQ][0])));
-    // (pi eps/4) phi_a h_l / sqrt(phi_a phi_l) * dphi_a/dt * (n_a . n_l) * n_a,d
-    const double w = RN_MUL(RN_MUL(RN_MUL(RN_MUL(kp.pi_eps_4, RN_MUL(RN_MUL(pb[a], hl), rsqrt(pal))), pd),
-                                   RN_MUL(RN_MUL(dot, ra), rl)),
-                            RN_MUL(gf[a][d], ra));
-    J0 = RN_FMA(w, RN_MUL(0.5, RN_ADD(lo.dcl[a][0], hi.dcl[a][0])), J0);
-    J1 = RN_FMA(w, RN_MUL(0.5, RN_ADD(lo.dcl[a][1], hi.dcl[a][1])), J1);
+    const double dot = RN_FMA(gfa[2], gfl[2], RN_FMA(gfa[1], gfl[1], RN_MUL(gfa[0], gfl[0])));
+    const double x = RN_MUL(RN_MUL(pal, gl2), RN_MUL(ga2, ga2));
+    double r;
+    if (x >= 0x1.0p-1000 && x <= 0x1.0p+1000) {
+      r = rsqrt(x);
+    } else {  // extreme magnitudes: factorised (never taken for O(1) fields)
+      const double ra = rsqrt(ga2);
+      r = RN_MUL(RN_MUL(rsqrt(pal), rsqrt(gl2)), RN_MUL(ra, ra));
+    }
+    const double w = RN_MUL(RN_MUL(RN_MUL(RN_MUL(kp.pi_eps_4, pb[a]), RN_MUL(hl, pd)), RN_MUL(dot, gfa[d])), r);
+    J0 = RN_FMA(w, RN_MUL(0.5, RN_ADD(lo.dcl(a, 0), hi.dcl(a, 0))), J0);
+    J1 = RN_FMA(w, RN_MUL(0.5, RN_ADD(lo.dcl(a, 1), hi.dcl(a, 1))), J1);
   }
   out[0] = RN_SUB(out[0], J0);
   out[1] = RN_SUB(out[1], J1);
+}
+
+struct MuQAcc {  // accessor over a register MuQ
+  const MuQ &q;
+  __device__ __forceinline__ double pn(int a) const { return q.pn[a]; }
+  __device__ __forceinline__ double dp(int a) const { return q.dp[a]; }
+  __device__ __forceinline__ double gt(int a, int e) const { return q.gn[a][e]; }
+  __device__ __forceinline__ double M(int c) const { return q.M[c]; }
+  __device__ __forceinline__ double mu(int c) const { return q.mu[c]; }
+  __device__ __forceinline__ double dcl(int a, int c) const { return q.dcl[a][c]; }
+};
+
+__device__ __forceinline__ void mu_face(const KParams &kp, const MuQ &lo, const MuQ &hi, int d, double out[NMU]) {
+  mu_face_t(kp, MuQAcc{lo}, MuQAcc{hi}, d, out);
 }
 
 // Cell part of the mu update (oracle O5.1-5.9) given phi^n, phi^{n+1}, mu^n of

@@ -34,6 +34,12 @@ __global__ void table_kernel(double *tab, int64_t nplanes, TabParams tp, int64_t
       row[T_MCHAT + a * 2 + c] = tp.m[a][c];
     }
   }
+  for (int a = 0; a < 3; ++a)
+    for (int c = 0; c < NMU; ++c) {
+      row[T_DI2A + a * 2 + c] = row[T_INV2A + LIQ * 2 + c] - row[T_INV2A + a * 2 + c];
+      row[T_DCHAT + a * 2 + c] = row[T_CHAT + LIQ * 2 + c] - row[T_CHAT + a * 2 + c];
+    }
+  row[TAB - 1] = 0.0;
 }
 
 void launch_table(cudaStream_t s, double *tab, int64_t nplanes, const TabParams &tp, int64_t step, int64_t zorig) {
