@@ -42,11 +42,6 @@ def _env_int(k, d):
         return d
 
 
-def decomp(n: int):
-    cfg = json.load(open(os.path.join(ROOT, "configs", f"{CONFIG}.json")))
-    return cfg, tuple(cfg["decomp"][str(n)])
-
-
 def flops_per_lup():
     from oracle import oracle as O
     from inputs import gen
@@ -156,26 +151,21 @@ def run_gpu(args):
     import torch
     import torch.distributed as dist
     from paper_1506_01684_b200 import pf
+    from paper_1506_01684_b200 import dist as pdist
 
-    world = _env_int("WORLD_SIZE", 1)
-    rank = _env_int("RANK", 0)
-    local = _env_int("LOCAL_RANK", 0)
+    rank, world, local = pdist.env_rank()
     n = args.gpus if world == 1 else world
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
-    cfg, (px, py, pz) = decomp(n)
+    cfg = json.load(open(os.path.join(ROOT, "configs", f"{CONFIG}.json")))
+    (NX, NY, NZ), (px, py, pz) = pdist.weak_grid(world if world > 1 else 1, per=512, config=CONFIG)
     from inputs import gen
     pd = gen.load_params("v1")
-    NX, NY, NZ = 512 * px, 512 * py, 512 * pz
     prm = pf.make_params(pd, cfg, nx=NX, ny=NY, nan_check_every=0)
-    nid = None
-    if world > 1:
-        obj = [pf.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nid = obj[0]
+    nid = pdist.share_from_rank0(pf.nccl_unique_id) if world > 1 else None
     stream = torch.cuda.Stream()
     ctx = pf.Context(NX, NY, NZ, prm, px, py, pz, rank=rank if world > 1 else 0, nranks=world,
                      device=local if world > 1 else 0, nccl_id=nid, stream=stream.cuda_stream)
@@ -187,11 +177,7 @@ def run_gpu(args):
             dist.barrier()
 
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return pdist.max_over_ranks(x, device="cuda")
 
     # warm-up
     ctx.step(args.warmup)
@@ -265,7 +251,7 @@ def run_gpu(args):
         if world == 1 and not args.no_cpu:
             cpu_v, cores, sample = cpu_oracle_sample(args.cpu_steps)
         line = {
-            "metric": "MLUP/s", "value": round(value, 2), "unit": "MLUP/s", "n_gpus": world if world > 1 else n,
+            "metric": "MLUP/s", "value": round(value, 2), "unit": "MLUP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Voronoi solid layer, PARAMS-v1)",

@@ -117,6 +117,14 @@ typedef struct pf_ctx pf_ctx;
 /* Fill out[128] with a fresh ncclUniqueId (call on rank 0 only). */
 pf_status pf_nccl_unique_id(uint8_t out[128]);
 
+/* Host-only query of the halo message plan (no GPU needed): for rank g->rank,
+ * the number of doubles it sends to (send_counts[r]) and receives from
+ * (recv_counts[r]) every rank r in one ghost-layer exchange of `field`
+ * (0 = phi, 4 components; 1 = mu, 2 components).  Faces and the 12 edges of
+ * every block; periodic x/y, zero-flux z.  Both arrays hold
+ * g->nranks entries (caller-owned).  Errors: PF_ERR_ARG, PF_ERR_CONFIG. */
+pf_status pf_halo_plan(const pf_grid *g, int32_t field, int64_t *send_counts, int64_t *recv_counts);
+
 /* Validate grid and parameters, select the device, allocate fields and
  * buffers, create the communicator (nranks > 1; collective over all ranks).
  * Errors: PF_ERR_CONFIG (divisibility, gamma not symmetric / non-positive,

@@ -568,6 +568,30 @@ pf_status pf_nccl_unique_id(uint8_t out[128]) {
   return PF_OK;
 }
 
+pf_status pf_halo_plan(const pf_grid *g, int32_t field, int64_t *send_counts, int64_t *recv_counts) {
+  if (!g || !send_counts || !recv_counts || (field != 0 && field != 1)) return PF_ERR_ARG;
+  if (g->px <= 0 || g->py <= 0 || g->pz <= 0 || g->nx % g->px || g->ny % g->py || g->nz % g->pz) return PF_ERR_CONFIG;
+  const int nb = g->px * g->py * g->pz;
+  if ((g->nranks != 1 && g->nranks != nb) || g->rank < 0 || g->rank >= g->nranks) return PF_ERR_CONFIG;
+  pf_ctx tmp;  // host-only: the region enumeration reads the grid alone
+  tmp.g = *g;
+  tmp.nblocks_total = nb;
+  const int nx = (int)(g->nx / g->px), ny = (int)(g->ny / g->py), nz = (int)(g->nz / g->pz);
+  const int ncomp = field == 0 ? NPH : NMU;
+  for (int r = 0; r < g->nranks; ++r) send_counts[r] = recv_counts[r] = 0;
+  for (int bid = 0; bid < nb; ++bid) {
+    const int bx = bid % g->px, by = (bid / g->px) % g->py, bz = bid / (g->px * g->py);
+    for (const auto &d : ghost_dirs()) {
+      const Region r = ghost_region(&tmp, bx, by, bz, d, nx, ny, nz);
+      const int rdst = owner_rank(&tmp, r.dst_bid), rsrc = owner_rank(&tmp, r.src_bid);
+      const int64_t n = r.ext[0] * r.ext[1] * r.ext[2] * ncomp;
+      if (rdst == g->rank && rsrc != g->rank) recv_counts[rsrc] += n;
+      if (rsrc == g->rank && rdst != g->rank) send_counts[rdst] += n;
+    }
+  }
+  return PF_OK;
+}
+
 pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
   g_create_error.clear();
   if (!g || !p || !out) return fail(nullptr, PF_ERR_ARG, "NULL argument");

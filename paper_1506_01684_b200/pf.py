@@ -25,7 +25,7 @@ I64 = ctypes.c_int64
 PF_OK, PF_ERR_CONFIG, PF_ERR_NUMERICAL, PF_ERR_CUDA, PF_ERR_COMM, PF_ERR_STATE, PF_ERR_ARG = 0, -1, -2, -3, -4, -5, -6
 STATUS_NAMES = {0: "PF_OK", -1: "PF_ERR_CONFIG", -2: "PF_ERR_NUMERICAL", -3: "PF_ERR_CUDA", -4: "PF_ERR_COMM",
                 -5: "PF_ERR_STATE", -6: "PF_ERR_ARG"}
-EXPORTS = ["pf_nccl_unique_id", "pf_create", "pf_init", "pf_write", "pf_set_time", "pf_step", "pf_read",
+EXPORTS = ["pf_nccl_unique_id", "pf_halo_plan", "pf_create", "pf_init", "pf_write", "pf_set_time", "pf_step", "pf_read",
            "pf_set_timing", "pf_info", "pf_last_error", "pf_destroy"]
 
 
@@ -72,6 +72,7 @@ def lib():
         L = ctypes.CDLL(LIB_PATH)
         vp = ctypes.c_void_p
         L.pf_nccl_unique_id.argtypes = [ctypes.POINTER(ctypes.c_uint8)]
+        L.pf_halo_plan.argtypes = [ctypes.POINTER(PfGrid), I32, ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.pf_create.argtypes = [ctypes.POINTER(PfGrid), ctypes.POINTER(PfParams), ctypes.POINTER(vp)]
         L.pf_init.argtypes = [vp, ctypes.c_uint64]
         L.pf_write.argtypes = [vp, vp, vp]
@@ -144,6 +145,19 @@ def nccl_unique_id() -> bytes:
     if st != PF_OK:
         raise PfError(st, "pf_nccl_unique_id failed")
     return bytes(buf)
+
+
+def halo_plan(nx, ny, nz, px, py, pz, rank, nranks, field):
+    """Host-only message plan of one ghost exchange: (send_counts, recv_counts)
+    in doubles per peer rank (pf_halo_plan; no GPU needed)."""
+    g = PfGrid()
+    g.nx, g.ny, g.nz, g.px, g.py, g.pz, g.rank, g.nranks = nx, ny, nz, px, py, pz, rank, nranks
+    snd = (I64 * nranks)()
+    rcv = (I64 * nranks)()
+    st = lib().pf_halo_plan(ctypes.byref(g), field, snd, rcv)
+    if st != PF_OK:
+        raise PfError(st, "pf_halo_plan")
+    return list(snd), list(rcv)
 
 
 def _ptr(x):
