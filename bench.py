@@ -133,8 +133,8 @@ def run_reference(args):
     steps, warm = args.steps, args.warmup
     from oracle import oracle as O  # noqa: F401  (builds the oracle)
     # each step: one oracle step over a bounded sample of the workload
-    _ = cpu_oracle_sample(max(0, min(warm, 1)), nz_slab=4) if warm else None
-    v, cores, sample = cpu_oracle_sample(steps, nz_slab=8)
+    _ = cpu_oracle_sample(max(0, min(warm, 1)), nz_slab=16) if warm else None
+    v, cores, sample = cpu_oracle_sample(steps, nz_slab=16)
     line = {"impl": "reference", "metric": "MLUP/s", "value": round(v, 3), "unit": "MLUP/s",
             "n_gpus": args.gpus, "steps": steps, "warmup": warm, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -249,7 +249,7 @@ def run_gpu(args):
             pass
         cpu_v, cores, sample = (None, None, "skipped")
         if world == 1 and not args.no_cpu:
-            cpu_v, cores, sample = cpu_oracle_sample(args.cpu_steps)
+            cpu_v, cores, sample = cpu_oracle_sample(args.cpu_steps, nz_slab=64)
         line = {
             "metric": "MLUP/s", "value": round(value, 2), "unit": "MLUP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
@@ -291,7 +291,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--cpu-steps", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
