@@ -2,12 +2,24 @@
 // runtime (pf_runtime.cu) and the kernel translation units.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include "pf_dev.cuh"
 
 namespace pf {
 
 constexpr int XO = 4;  // column of interior i = 0 within a padded row (i = -1 at 3)
+constexpr int TILE_X = 32, TILE_Y = 8;  // CTA tile of the z-marching sweeps (pf_tile.cuh)
+
+// TMA descriptors of one block's fields in one time level (encoded on the host
+// over the whole padded allocation: dims {pitch, ny+2, planes}, x fastest).
+// tile: box (TX+2) x (TY+2) x 1 — interior tile + ring; int: box TX x TY x 1.
+struct TmaMaps {
+  CUtensorMap phi[NPH];   // phi^n,     tile box
+  CUtensorMap phin[NPH];  // phi^{n+1}, tile box
+  CUtensorMap mu[NMU];    // mu^n,      tile box
+  CUtensorMap mui[NMU];   // mu^n,      interior box
+};
 
 // Pointers into one block's fields, offset to interior cell (0,0,0) of the
 // current window position; element (i,j,k) at p + k*plane + j*pitch + i with
@@ -20,6 +32,7 @@ struct BlockView {
   int nx, ny, nz;
   int64_t pitch, plane;
   const double *tab;        // table row of local plane k = 0
+  int zoff;                 // allocation plane of local k = 0 (1 + window offset), for TMA
 };
 
 // Strided 3D box copy (halo exchange: local copy, pack, unpack).
@@ -51,8 +64,8 @@ struct TabParams {
 void launch_table(cudaStream_t s, double *tab, int64_t nplanes, const TabParams &tp, int64_t step, int64_t zorig);
 void launch_phi_naive(cudaStream_t s, const KParams &kp, const BlockView &b);
 void launch_mu_naive(cudaStream_t s, const KParams &kp, const BlockView &b);
-void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b);
-void launch_mu_tiled(cudaStream_t s, const KParams &kp, const BlockView &b);
+void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm);
+void launch_mu_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm);
 void launch_copy(cudaStream_t s, const CopyOp *d_ops, int nops, int64_t max_cells);
 void launch_init(cudaStream_t s, const InitSpec &is, double *const phi[NPH], double *const mu[NMU],
                  int nx, int ny, int nz, int64_t pitch, int64_t plane, int64_t x0, int64_t y0, int64_t z0);

@@ -2,57 +2,62 @@
 // 2.5D tiles; every staggered value M grad mu - J_at (the
 // "computationally most intensive part") is evaluated once per face.
 //
-// Shared memory per CTA (2 CTAs / SM):
-//   * phi^{n+1} tile planes k-1 .. k+2 (ring + corners: the D3C19 stencil of the
-//     anti-trapping current needs tangential gradients at face neighbours,
-//     PAPER.md:179), phi^n and mu tile planes k .. k+2, table rows — all staged
-//     two planes ahead with cp.async;
-//   * the mobility of plane k (computed once per cell);
-//   * the x/y face values of plane k.
+// Shared memory per CTA (2 CTAs / SM), filled by TMA bulk-tensor copies issued
+// by one thread and guarded by mbarriers:
+//   * phi^{n+1} tile planes k-1 .. k+2 (interior + ring + corners: the D3C19
+//     stencil of the anti-trapping current needs tangential gradients at face
+//     neighbours) — staged two planes ahead, 4 slots;
+//   * phi^n and mu tile planes k, k+1 — staged one plane ahead, 2 slots;
+//   * table rows; the mobility of plane k (computed once per cell); the x/y
+//     face values of plane k.
 // Everything else a face needs (dphi, c^l - c^a, tangential gradients) is
-// read or derived from the staged planes inside the face routine, and only
-// when the exact-zero guards let the anti-trapping term through (bulk liquid
-// and bulk solid faces exit after the diffusive flux).  z-faces are carried in
-// registers.  All arithmetic is the pinned code of pf_dev.cuh, so results do
-// not depend on tile or block boundaries.
+// derived from the staged planes inside the face routine, and only when the
+// exact-zero guards let the anti-trapping term through.  z-faces are carried
+// in registers; the own column's phi^n / mu at k+1 (the z-face's upper cell)
+// come from registers.  All arithmetic is the pinned code of pf_dev.cuh, so
+// results do not depend on tile or block boundaries.
 #include "pf_tile.cuh"
 
 namespace pf {
 
-constexpr int NS3 = 3;  // phi^n / mu slots: k, k+1, k+2 (in flight)
-
-struct MuSmem {
-  double pn[NSLOT][NPH][RY][RX];  // phi^{n+1}, planes k-1 .. k+2
-  double po[NS3][NPH][RY][RX];    // phi^n, planes k .. k+2
-  double mu[NS3][NMU][RY][RX];    // mu^n,  planes k .. k+2
+struct __align__(128) MuSmem {
+  double pn[NSLOT][NPH][TSZ];     // phi^{n+1}, planes k-1 .. k+2
+  double po[2][NPH][TSZ];         // phi^n, planes k, k+1
+  double mu[2][NMU][TSZ];         // mu^n,  planes k, k+1
   double tab[NSLOT][TAB];
   double M[NMU][RY][RX];          // mobility of plane k
   double fx[NMU][TY][TX + 1];     // x-face values at i - 1/2
   double fy[NMU][TY + 1][TX];     // y-face values at j - 1/2
+  uint64_t bar_pn[NSLOT];         // phi^{n+1} + table of a plane
+  uint64_t bar_pm[2];             // phi^n + mu of a plane
 };
+#define T(arr, row, col) TILE_AT(arr, row, col)
+constexpr uint32_t MU_PN_BYTES = (NPH * RXS * RY + TAB) * 8;   // phi^{n+1} tiles + table row
+constexpr uint32_t MU_PM_BYTES = ((NPH + NMU) * RXS * RY) * 8;  // phi^n + mu tiles
 
 // Accessor over the staged planes for tile cell (col,row) of plane k:
-// pn slots (k-1, k, k+1) = (snm, sn, snp), phi^n/mu slot s3, table row tab.
+// phi^{n+1} slots (k-1, k, k+1) = (snm, sn, snp), phi^n/mu slot s2, table row.
 struct RawQ {
   const MuSmem &S;
   const KParams &kp;
-  int snm, sn, snp, s3, col, row;
+  int snm, sn, snp, s2, col, row;
   const double *tab;
   double Mv[NMU];
-  __device__ __forceinline__ double pn(int a) const { return S.pn[sn][a][row][col]; }
-  __device__ __forceinline__ double dp(int a) const { return RN_SUB(S.pn[sn][a][row][col], S.po[s3][a][row][col]); }
+  __device__ __forceinline__ double pn(int a) const { return T(S.pn[sn][a], row, col); }
+  __device__ __forceinline__ double dp(int a) const { return RN_SUB(T(S.pn[sn][a], row, col), T(S.po[s2][a], row, col)); }
   __device__ __forceinline__ double gt(int a, int e) const {
-    if (e == 0) return cgrad(kp, S.pn[sn][a][row][col - 1], S.pn[sn][a][row][col + 1]);
-    if (e == 1) return cgrad(kp, S.pn[sn][a][row - 1][col], S.pn[sn][a][row + 1][col]);
-    return cgrad(kp, S.pn[snm][a][row][col], S.pn[snp][a][row][col]);
+    if (e == 0) return cgrad(kp, T(S.pn[sn][a], row, col - 1), T(S.pn[sn][a], row, col + 1));
+    if (e == 1) return cgrad(kp, T(S.pn[sn][a], row - 1, col), T(S.pn[sn][a], row + 1, col));
+    return cgrad(kp, T(S.pn[snm][a], row, col), T(S.pn[snp][a], row, col));
   }
   __device__ __forceinline__ double M(int c) const { return Mv[c]; }
-  __device__ __forceinline__ double mu(int c) const { return S.mu[s3][c][row][col]; }
+  __device__ __forceinline__ double mu(int c) const { return T(S.mu[s2][c], row, col); }
   __device__ __forceinline__ double dcl(int a, int c) const { return dcl_of(tab, a, c, mu(c)); }
 };
 
-__global__ void __launch_bounds__(NTHR, 2) mu_tiled_kernel(KParams kp, BlockView b, int kz) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__global__ void __launch_bounds__(NTHR, 2) mu_tiled_kernel(const __grid_constant__ TmaMaps tm, KParams kp,
+                                                           BlockView b, int kz) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   MuSmem &S = *reinterpret_cast<MuSmem *>(smem_raw);
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
   const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
@@ -66,97 +71,113 @@ __global__ void __launch_bounds__(NTHR, 2) mu_tiled_kernel(KParams kp, BlockView
   int rcol = 0, rrow = 0;
   if (ring_thr) ring_cell(tid, rcol, rrow);
   const bool rcorner = ring_corner(rcol, rrow);
-  const int rgi = i0 - 1 + rcol, rgj = j0 - 1 + rrow;
-  const bool rok = ring_thr && rgi <= b.nx && rgj <= b.ny;
-  const int64_t roff = rok ? (int64_t)rgj * b.pitch + rgi : colo;
 
   auto slot = [&](int k) { return (k - k0 + 1) & (NSLOT - 1); };
-  auto slot3 = [&](int k) { return (k - k0 + 3) % NS3; };
-  // stage plane k: phi^{n+1} (tile + ring + corners) always; phi^n, mu and the
-  // mu when plane k is >= k0 (the first plane whose cells we update)
-  auto stage = [&](int k) {
-    const int s = slot(k), s3 = slot3(k);
-    const int64_t pk = (int64_t)k * b.plane;
-    const bool full = k >= k0;
+  auto par4 = [&](int k) { return (uint32_t)(((k - k0 + 1) >> 2) & 1); };
+  auto slot2 = [&](int k) { return (k - k0) & 1; };
+  auto par2 = [&](int k) { return (uint32_t)(((k - k0) >> 1) & 1); };
+  const int bx = i0 - 2 + XO, by = j0;  // tile box origin (16-byte aligned x)
+  auto stage_pn = [&](int k) {            // phi^{n+1} tiles + table row of plane k
+    const int s = slot(k);
+    fence_proxy_async();
+    mbar_expect_tx(&S.bar_pn[s], MU_PN_BYTES);
 #pragma unroll
-    for (int a = 0; a < NPH; ++a) {
-      cp_async8(&S.pn[s][a][orow][oc], b.phin[a] + pk + colo, inb);
-      if (ring_thr) cp_async8(&S.pn[s][a][rrow][rcol], b.phin[a] + pk + roff, rok);
-      if (full) {
-        cp_async8(&S.po[s3][a][orow][oc], b.phi[a] + pk + colo, inb);
-        if (ring_thr && !rcorner) cp_async8(&S.po[s3][a][rrow][rcol], b.phi[a] + pk + roff, rok);
-      }
-    }
-    if (full) {
+    for (int a = 0; a < NPH; ++a) tma_load_3d(S.pn[s][a], &tm.phin[a], bx, by, k + b.zoff, &S.bar_pn[s]);
+    bulk_load(S.tab[s], b.tab + (int64_t)k * TAB, TAB * 8, &S.bar_pn[s]);
+  };
+  auto stage_pm = [&](int k) {            // phi^n and mu tiles of plane k
+    const int s = slot2(k);
+    fence_proxy_async();
+    mbar_expect_tx(&S.bar_pm[s], MU_PM_BYTES);
 #pragma unroll
-      for (int c = 0; c < NMU; ++c) {
-        cp_async8(&S.mu[s3][c][orow][oc], b.mu[c] + pk + colo, inb);
-        if (ring_thr && !rcorner) cp_async8(&S.mu[s3][c][rrow][rcol], b.mu[c] + pk + roff, rok);
-      }
-    }
-    if (tid < TAB) cp_async8(&S.tab[s][tid], b.tab + (int64_t)k * TAB + tid, true);
-    cp_async_commit();
+    for (int a = 0; a < NPH; ++a) tma_load_3d(S.po[s][a], &tm.phi[a], bx, by, k + b.zoff, &S.bar_pm[s]);
+#pragma unroll
+    for (int c = 0; c < NMU; ++c) tma_load_3d(S.mu[s][c], &tm.mu[c], bx, by, k + b.zoff, &S.bar_pm[s]);
   };
   auto rawq = [&](int k, int col, int row) {
-    return RawQ{S, kp, slot(k - 1), slot(k), slot(k + 1), slot3(k), col, row, S.tab[slot(k)], {0.0, 0.0}};
+    return RawQ{S, kp, slot(k - 1), slot(k), slot(k + 1), slot2(k), col, row, S.tab[slot(k)], {0.0, 0.0}};
   };
-
-  // ---- prologue: planes k0-1 .. k0+1 resident
-  stage(k0 - 1);
-  stage(k0);
-  stage(k0 + 1);
-  cp_async_wait<0>();
-  __syncthreads();
-  // z-face k0 - 1/2 from the own column's quantities at k0-1 and k0 (phi^n,
-  // mu, table at k0-1 read directly from global: needed once per chunk)
-  double fzm[NMU];
-  {
-    double po[NPH], pn[NPH], mu[NMU];
-    const int64_t pk = (int64_t)(k0 - 1) * b.plane;
+  // own column phi^n, mu of plane k from global (registers)
+  auto own_load = [&](int k, double po[NPH], double mu[NMU]) {
+    const int64_t pk = (int64_t)k * b.plane;
 #pragma unroll
-    for (int a = 0; a < NPH; ++a) { po[a] = inb ? __ldg(b.phi[a] + pk + colo) : 0.0; pn[a] = S.pn[slot(k0 - 1)][a][orow][oc]; }
+    for (int a = 0; a < NPH; ++a) po[a] = inb ? __ldg(b.phi[a] + pk + colo) : 0.0;
 #pragma unroll
     for (int c = 0; c < NMU; ++c) mu[c] = inb ? __ldg(b.mu[c] + pk + colo) : 0.0;
-    MuQ qm;
-    mu_cell_q(S.tab[slot(k0 - 1)], po, pn, mu, qm);
-    const int s0 = slot(k0 - 1);
+  };
+  // own-column MuQ of plane k in registers (tangential x,y gradients from slot(k))
+  auto own_q = [&](int k, const double po[NPH], const double mu[NMU], MuQ &q) {
+    const int sc = slot(k);
+    double pn[NPH];
+#pragma unroll
+    for (int a = 0; a < NPH; ++a) pn[a] = T(S.pn[sc][a], orow, oc);
+    mu_cell_q(S.tab[sc], po, pn, mu, q);
 #pragma unroll
     for (int a = 0; a < NPH; ++a) {
-      qm.gn[a][0] = cgrad(kp, S.pn[s0][a][orow][oc - 1], S.pn[s0][a][orow][oc + 1]);
-      qm.gn[a][1] = cgrad(kp, S.pn[s0][a][orow - 1][oc], S.pn[s0][a][orow + 1][oc]);
-      qm.gn[a][2] = 0.0;
+      q.gn[a][0] = cgrad(kp, T(S.pn[sc][a], orow, oc - 1), T(S.pn[sc][a], orow, oc + 1));
+      q.gn[a][1] = cgrad(kp, T(S.pn[sc][a], orow - 1, oc), T(S.pn[sc][a], orow + 1, oc));
+      q.gn[a][2] = 0.0;
     }
-    RawQ hi = rawq(k0, oc, orow);
-    double poc[NPH];
-#pragma unroll
-    for (int a = 0; a < NPH; ++a) poc[a] = S.po[slot3(k0)][a][orow][oc];
-    hi.Mv[0] = mob_of(hi.tab, 0, poc);
-    hi.Mv[1] = mob_of(hi.tab, 1, poc);
-    mu_face_t(kp, MuQAcc{qm}, hi, 2, fzm);
+  };
+
+  // ---- prologue: phi^{n+1} planes k0-1 .. k0+1, phi^n / mu plane k0
+  if (tid == 0) {
+    for (int q = 0; q < NSLOT; ++q) mbar_init(&S.bar_pn[q], 1);
+    for (int q = 0; q < 2; ++q) mbar_init(&S.bar_pm[q], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    stage_pn(k0 - 1);
+    stage_pn(k0);
+    stage_pn(k0 + 1);
+    stage_pm(k0);
+  }
+  double fzm[NMU], po_n[NPH], mu_n[NMU];
+  {  // z-face k0 - 1/2 from the own column's register quantities at k0-1 and k0
+    double pom[NPH], mum[NMU];
+    own_load(k0 - 1, pom, mum);
+    own_load(k0, po_n, mu_n);
+    mbar_wait(&S.bar_pn[slot(k0 - 1)], par4(k0 - 1));
+    mbar_wait(&S.bar_pn[slot(k0)], par4(k0));
+    mbar_wait(&S.bar_pn[slot(k0 + 1)], par4(k0 + 1));
+    MuQ qm, qc;
+    own_q(k0 - 1, pom, mum, qm);
+    own_q(k0, po_n, mu_n, qc);
+    mu_face(kp, qm, qc, 2, fzm);
   }
 
   for (int k = k0; k < k1; ++k) {
-    const int sn = slot(k), s3 = slot3(k);
-    // A: mobility of plane k (own + ring cells), then stage plane k+2
-    {
+    const int sn = slot(k), s2 = slot2(k);
+    const bool more = k + 1 < k1;
+    // A: stage phi^{n+1}(k+2) and phi^n/mu(k+1) (their slots were last read in
+    // D(k-1), before barrier E(k-1)); own column of plane k+1 into registers
+    if (tid == 0) {
+      if (k + 2 <= k1) stage_pn(k + 2);
+      if (more) stage_pm(k + 1);
+    }
+    double po_c[NPH], mu_c[NMU];
+#pragma unroll
+    for (int a = 0; a < NPH; ++a) po_c[a] = po_n[a];
+#pragma unroll
+    for (int c = 0; c < NMU; ++c) mu_c[c] = mu_n[c];
+    own_load(k + 1, po_n, mu_n);
+    mbar_wait(&S.bar_pm[s2], par2(k));   // phi^n / mu of plane k resident
+    {  // mobility of plane k (own + ring cells)
       double po[NPH];
 #pragma unroll
-      for (int a = 0; a < NPH; ++a) po[a] = S.po[s3][a][orow][oc];
+      for (int a = 0; a < NPH; ++a) po[a] = T(S.po[s2][a], orow, oc);
       S.M[0][orow][oc] = mob_of(S.tab[sn], 0, po);
       S.M[1][orow][oc] = mob_of(S.tab[sn], 1, po);
       if (ring_thr && !rcorner) {
 #pragma unroll
-        for (int a = 0; a < NPH; ++a) po[a] = S.po[s3][a][rrow][rcol];
+        for (int a = 0; a < NPH; ++a) po[a] = T(S.po[s2][a], rrow, rcol);
         S.M[0][rrow][rcol] = mob_of(S.tab[sn], 0, po);
         S.M[1][rrow][rcol] = mob_of(S.tab[sn], 1, po);
       }
     }
-    if (k + 2 <= k1) stage(k + 2);
-    else cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();  // C
+    __syncthreads();  // C: M of plane k visible; faces of plane k-1 consumed
     // D: faces of plane k
-    double po_c[NPH], pn_c[NPH], mu_c[NMU];
     {
       double f[NMU];
       {  // own -x face
@@ -187,24 +208,18 @@ __global__ void __launch_bounds__(NTHR, 2) mu_tiled_kernel(KParams kp, BlockView
         else { S.fy[0][TY][c0 - 1] = f[0]; S.fy[1][TY][c0 - 1] = f[1]; }
       }
     }
-    double fzp[NMU];
-    {  // z-face k+1/2 of the own column; own values of plane k to registers
-      RawQ lo = rawq(k, oc, orow), hi = rawq(k + 1, oc, orow);
+    double fzp[NMU], pn_c[NPH];
+    {  // z-face k+1/2: own cell at k (shared memory) and at k+1 (registers)
+      RawQ lo = rawq(k, oc, orow);
       lo.Mv[0] = S.M[0][orow][oc]; lo.Mv[1] = S.M[1][orow][oc];
-      double pon[NPH];
+      MuQ qn;
+      own_q(k + 1, po_n, mu_n, qn);
+      mu_face_t(kp, lo, MuQAcc{qn}, 2, fzp);
 #pragma unroll
-      for (int a = 0; a < NPH; ++a) {
-        pon[a] = S.po[slot3(k + 1)][a][orow][oc];
-        po_c[a] = S.po[s3][a][orow][oc];
-        pn_c[a] = S.pn[sn][a][orow][oc];
-      }
-      mu_c[0] = S.mu[s3][0][orow][oc];
-      mu_c[1] = S.mu[s3][1][orow][oc];
-      hi.Mv[0] = mob_of(hi.tab, 0, pon);
-      hi.Mv[1] = mob_of(hi.tab, 1, pon);
-      mu_face_t(kp, lo, hi, 2, fzp);
+      for (int a = 0; a < NPH; ++a) pn_c[a] = T(S.pn[sn][a], orow, oc);
     }
     __syncthreads();  // E
+    if (k + 2 <= k1) mbar_wait(&S.bar_pn[slot(k + 2)], par4(k + 2));  // for the next iteration
     // F: cell update of (i, j, k)
     if (active) {
       double divf[NMU], out[NMU];
@@ -220,16 +235,17 @@ __global__ void __launch_bounds__(NTHR, 2) mu_tiled_kernel(KParams kp, BlockView
     fzm[0] = fzp[0];
     fzm[1] = fzp[1];
   }
+#undef T
 }
 
-void launch_mu_tiled(cudaStream_t s, const KParams &kp, const BlockView &b) {
+void launch_mu_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm) {
   const int gx = (b.nx + TX - 1) / TX, gy = (b.ny + TY - 1) / TY;
   const int kz = chunk_z(b.nz, gx * gy);
   dim3 grd(gx, gy, (b.nz + kz - 1) / kz), blk(TX, TY);
   const size_t sm = sizeof(MuSmem);
   static bool attr = false;
   if (!attr) { cudaFuncSetAttribute(mu_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr = true; }
-  mu_tiled_kernel<<<grd, blk, sm, s>>>(kp, b, kz);
+  mu_tiled_kernel<<<grd, blk, sm, s>>>(tm, kp, b, kz);
 }
 
 }  // namespace pf

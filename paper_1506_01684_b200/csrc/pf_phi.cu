@@ -6,65 +6,64 @@
 //     by both adjacent cells;
 //   * z-faces: carried in registers from k-1/2 to k+1/2 (the paper's Nx x Ny
 //     staggered buffer becomes one register set per column).
-// Data movement: tile planes (interior + ring), mu and the per-plane table row
-// are staged two planes ahead with cp.async into 4 rotating slots; each plane
-// costs two CTA barriers.  The face and gradient routines are the pinned ones
-// of pf_dev.cuh: a face evaluated at a tile / chunk / block edge has the same
-// bits as mid-tile.
+// Data movement: per plane, one elected thread issues TMA bulk-tensor copies of
+// the 4 phi tiles (interior + ring, (TX+2) x (TY+2) boxes), the 2 mu interior
+// boxes and a bulk copy of the table row, two planes ahead, into 4 rotating
+// slots guarded by mbarriers.  Two CTA barriers per plane.  The face and
+// gradient routines are the pinned ones of pf_dev.cuh: a face evaluated at a
+// tile / chunk / block edge has the same bits as mid-tile.
 #include "pf_tile.cuh"
 
 namespace pf {
 
-struct PhiSmem {
-  double p[NSLOT][NPH][RY][RX];   // phi^n tile planes (ring incl. corners)
-  double mu[NSLOT][NMU][TY][TX];  // mu^n of the interior cells
-  double tab[NSLOT][TAB];         // per-plane table rows
-  double fx[NPH][TY][TX + 1];     // x-face fluxes at i - 1/2, i = 0..TX
-  double fy[NPH][TY + 1][TX];     // y-face fluxes at j - 1/2, j = 0..TY
+struct __align__(128) PhiSmem {
+  double p[NSLOT][NPH][TSZ];       // phi^n tile planes, (row, col) at row * RX + col
+  double mu[NSLOT][NMU][TY * TX];  // mu^n of the interior cells
+  double tab[NSLOT][TAB];          // per-plane table rows
+  double fx[NPH][TY][TX + 1];      // x-face fluxes at i - 1/2, i = 0..TX
+  double fy[NPH][TY + 1][TX];      // y-face fluxes at j - 1/2, j = 0..TY
+  uint64_t bar[NSLOT];             // one mbarrier per slot
 };
 
+constexpr uint32_t PHI_STAGE_BYTES = (NPH * RXS * RY + NMU * TX * TY + TAB) * 8;
+
 template <bool ANISO>
-__global__ void __launch_bounds__(NTHR, 2) phi_tiled_kernel(KParams kp, BlockView b, int kz) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__global__ void __launch_bounds__(NTHR, 2) phi_tiled_kernel(const __grid_constant__ TmaMaps tm, KParams kp, BlockView b,
+                                                            int kz) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   PhiSmem &S = *reinterpret_cast<PhiSmem *>(smem_raw);
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
   const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
   const int k0 = blockIdx.z * kz, k1 = min(k0 + kz, b.nz);
   const int i = i0 + tx, j = j0 + ty;
   const bool active = (i < b.nx) && (j < b.ny);   // owns an interior cell
-  const bool inb = (i <= b.nx) && (j <= b.ny);     // interior or ghost column
   const int64_t colo = (int64_t)j * b.pitch + i;
   const int oc = tx + 1, orow = ty + 1;            // own tile coordinates
-  const bool ring_thr = tid < NRING;
-  int rcol = 0, rrow = 0;
-  if (ring_thr) ring_cell(tid, rcol, rrow);
-  const int rgi = i0 - 1 + rcol, rgj = j0 - 1 + rrow;
-  const bool rok = ring_thr && rgi <= b.nx && rgj <= b.ny && (ANISO || !ring_corner(rcol, rrow));
-  const int64_t roff = rok ? (int64_t)rgj * b.pitch + rgi : colo;
+#define T(arr, row, col) TILE_AT(arr, row, col)
 
   auto slot = [&](int k) { return (k - k0 + 1) & (NSLOT - 1); };
-  // stage plane k (tile + ring, mu, table row) into its slot
+  auto parity = [&](int k) { return (uint32_t)(((k - k0 + 1) >> 2) & 1); };
+  // plane k -> its slot: 4 phi tiles, 2 mu interior boxes, the table row
   auto stage = [&](int k) {
     const int s = slot(k);
-    const int64_t pk = (int64_t)k * b.plane;
+    fence_proxy_async();
+    mbar_expect_tx(&S.bar[s], PHI_STAGE_BYTES);
+    const int z = k + b.zoff;
 #pragma unroll
-    for (int a = 0; a < NPH; ++a) {
-      cp_async8(&S.p[s][a][orow][oc], b.phi[a] + pk + colo, inb);
-      if (ring_thr) cp_async8(&S.p[s][a][rrow][rcol], b.phi[a] + pk + roff, rok);
-    }
+    for (int a = 0; a < NPH; ++a) tma_load_3d(S.p[s][a], &tm.phi[a], i0 - 2 + XO, j0, z, &S.bar[s]);
 #pragma unroll
-    for (int c = 0; c < NMU; ++c) cp_async8(&S.mu[s][c][ty][tx], b.mu[c] + pk + colo, active);
-    if (tid < TAB) cp_async8(&S.tab[s][tid], b.tab + (int64_t)k * TAB + tid, true);
-    cp_async_commit();
+    for (int c = 0; c < NMU; ++c) tma_load_3d(S.mu[s][c], &tm.mui[c], i0 + XO, j0 + 1, z, &S.bar[s]);
+    bulk_load(S.tab[s], b.tab + (int64_t)k * TAB, TAB * 8, &S.bar[s]);
   };
+  auto wait = [&](int k) { mbar_wait(&S.bar[slot(k)], parity(k)); };
   // tangential centre gradients of tile cell (col,row) in slot sc (component
   // d unused); z-tangential from slots sm/sp
   auto tan_grad = [&](int sc, int sm, int sp, int col, int row, int d, double g[NPH][3]) {
 #pragma unroll
     for (int a = 0; a < NPH; ++a) {
-      g[a][0] = d == 0 ? 0.0 : cgrad(kp, S.p[sc][a][row][col - 1], S.p[sc][a][row][col + 1]);
-      g[a][1] = d == 1 ? 0.0 : cgrad(kp, S.p[sc][a][row - 1][col], S.p[sc][a][row + 1][col]);
-      g[a][2] = d == 2 ? 0.0 : cgrad(kp, S.p[sm][a][row][col], S.p[sp][a][row][col]);
+      g[a][0] = d == 0 ? 0.0 : cgrad(kp, T(S.p[sc][a], row, col - 1), T(S.p[sc][a], row, col + 1));
+      g[a][1] = d == 1 ? 0.0 : cgrad(kp, T(S.p[sc][a], row - 1, col), T(S.p[sc][a], row + 1, col));
+      g[a][2] = d == 2 ? 0.0 : cgrad(kp, T(S.p[sm][a], row, col), T(S.p[sp][a], row, col));
     }
   };
   double gdum[NPH][3];
@@ -74,17 +73,24 @@ __global__ void __launch_bounds__(NTHR, 2) phi_tiled_kernel(KParams kp, BlockVie
     for (int e = 0; e < 3; ++e) gdum[a][e] = 0.0;
 
   // ---- prologue: planes k0-1, k0, k0+1 resident, z-face k0 - 1/2
-  stage(k0 - 1);
-  stage(k0);
-  stage(k0 + 1);
-  cp_async_wait<0>();
+  if (tid == 0) {
+    for (int s = 0; s < NSLOT; ++s) mbar_init(&S.bar[s], 1);
+    mbar_fence_init();
+  }
   __syncthreads();
+  if (tid == 0) {
+    stage(k0 - 1);
+    stage(k0);
+    stage(k0 + 1);
+  }
+  wait(k0 - 1);
+  wait(k0);
   double jzm[NPH];
   {
     const int s0 = slot(k0 - 1), s1 = slot(k0);
     double lo[NPH], hi[NPH], gl[NPH][3], gh[NPH][3];
 #pragma unroll
-    for (int a = 0; a < NPH; ++a) { lo[a] = S.p[s0][a][orow][oc]; hi[a] = S.p[s1][a][orow][oc]; }
+    for (int a = 0; a < NPH; ++a) { lo[a] = T(S.p[s0][a], orow, oc); hi[a] = T(S.p[s1][a], orow, oc); }
     if (ANISO) {
       tan_grad(s0, s0, s0, oc, orow, 2, gl);
       tan_grad(s1, s1, s1, oc, orow, 2, gh);
@@ -93,11 +99,10 @@ __global__ void __launch_bounds__(NTHR, 2) phi_tiled_kernel(KParams kp, BlockVie
   }
 
   for (int k = k0; k < k1; ++k) {
-    // A: stage plane k+2 (needed from iteration k+1 on)
-    if (k + 2 <= k1) stage(k + 2);
-    else cp_async_commit();      // keep the group count uniform
-    cp_async_wait<1>();          // plane k+1 landed (this thread's copies)
-    __syncthreads();             // C: ... and everybody's
+    // A: stage plane k+2 (needed from iteration k+1 on); wait for plane k+1
+    if (tid == 0 && k + 2 <= k1) stage(k + 2);
+    wait(k + 1);
+    __syncthreads();  // C: faces of plane k-1 consumed by everybody
     const int sc = slot(k), sm = slot(k - 1), sp = slot(k + 1);
     // D: faces of plane k; own column values to registers
     double pm[NPH], pc[NPH], pp[NPH], jzp[NPH];
@@ -107,7 +112,7 @@ __global__ void __launch_bounds__(NTHR, 2) phi_tiled_kernel(KParams kp, BlockVie
       for (int d = 0; d < 2; ++d) {   // own -x (d = 0) and -y (d = 1) face
         const int lc = d == 0 ? oc - 1 : oc, lr = d == 0 ? orow : orow - 1;
 #pragma unroll
-        for (int a = 0; a < NPH; ++a) { lo[a] = S.p[sc][a][lr][lc]; hi[a] = S.p[sc][a][orow][oc]; }
+        for (int a = 0; a < NPH; ++a) { lo[a] = T(S.p[sc][a], lr, lc); hi[a] = T(S.p[sc][a], orow, oc); }
         if (ANISO) {
           tan_grad(sc, sm, sp, lc, lr, d, gl);
           tan_grad(sc, sm, sp, oc, orow, d, gh);
@@ -125,7 +130,7 @@ __global__ void __launch_bounds__(NTHR, 2) phi_tiled_kernel(KParams kp, BlockVie
         const int c0 = d == 1 ? tid + 1 : TX, r0 = d == 1 ? TY : tid - TX + 1;
         const int c1 = d == 1 ? c0 : c0 + 1, r1 = d == 1 ? r0 + 1 : r0;
 #pragma unroll
-        for (int a = 0; a < NPH; ++a) { lo[a] = S.p[sc][a][r0][c0]; hi[a] = S.p[sc][a][r1][c1]; }
+        for (int a = 0; a < NPH; ++a) { lo[a] = T(S.p[sc][a], r0, c0); hi[a] = T(S.p[sc][a], r1, c1); }
         if (ANISO) {
           tan_grad(sc, sm, sp, c0, r0, d, gl);
           tan_grad(sc, sm, sp, c1, r1, d, gh);
@@ -140,9 +145,9 @@ __global__ void __launch_bounds__(NTHR, 2) phi_tiled_kernel(KParams kp, BlockVie
       // z-face k+1/2 (own column)
 #pragma unroll
       for (int a = 0; a < NPH; ++a) {
-        pm[a] = S.p[sm][a][orow][oc];
-        pc[a] = S.p[sc][a][orow][oc];
-        pp[a] = S.p[sp][a][orow][oc];
+        pm[a] = T(S.p[sm][a], orow, oc);
+        pc[a] = T(S.p[sc][a], orow, oc);
+        pp[a] = T(S.p[sp][a], orow, oc);
       }
       if (ANISO) {
         tan_grad(sc, sc, sc, oc, orow, 2, gl);
@@ -156,14 +161,14 @@ __global__ void __launch_bounds__(NTHR, 2) phi_tiled_kernel(KParams kp, BlockVie
       double gc[NPH][3], dsum[NPH], mu[NMU], out[NPH];
 #pragma unroll
       for (int a = 0; a < NPH; ++a) {
-        gc[a][0] = cgrad(kp, S.p[sc][a][orow][oc - 1], S.p[sc][a][orow][oc + 1]);
-        gc[a][1] = cgrad(kp, S.p[sc][a][orow - 1][oc], S.p[sc][a][orow + 1][oc]);
+        gc[a][0] = cgrad(kp, T(S.p[sc][a], orow, oc - 1), T(S.p[sc][a], orow, oc + 1));
+        gc[a][1] = cgrad(kp, T(S.p[sc][a], orow - 1, oc), T(S.p[sc][a], orow + 1, oc));
         gc[a][2] = cgrad(kp, pm[a], pp[a]);
         dsum[a] = ((S.fx[a][ty][tx + 1] - S.fx[a][ty][tx]) + (S.fy[a][ty + 1][tx] - S.fy[a][ty][tx])) +
                   (jzp[a] - jzm[a]);
       }
-      mu[0] = S.mu[sc][0][ty][tx];
-      mu[1] = S.mu[sc][1][ty][tx];
+      mu[0] = S.mu[sc][0][ty * TX + tx];
+      mu[1] = S.mu[sc][1][ty * TX + tx];
       phi_cell_update_div(kp, S.tab[sc], pc, mu, gc, dsum, out);
       const int64_t o = (int64_t)k * b.plane + colo;
 #pragma unroll
@@ -172,9 +177,10 @@ __global__ void __launch_bounds__(NTHR, 2) phi_tiled_kernel(KParams kp, BlockVie
 #pragma unroll
     for (int a = 0; a < NPH; ++a) jzm[a] = jzp[a];
   }
+#undef T
 }
 
-void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b) {
+void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm) {
   const int gx = (b.nx + TX - 1) / TX, gy = (b.ny + TY - 1) / TY;
   const int kz = chunk_z(b.nz, gx * gy);
   dim3 grd(gx, gy, (b.nz + kz - 1) / kz), blk(TX, TY);
@@ -182,10 +188,10 @@ void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b) {
   static bool attr[2] = {false, false};
   if (kp.aniso) {
     if (!attr[1]) { cudaFuncSetAttribute(phi_tiled_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr[1] = true; }
-    phi_tiled_kernel<true><<<grd, blk, sm, s>>>(kp, b, kz);
+    phi_tiled_kernel<true><<<grd, blk, sm, s>>>(tm, kp, b, kz);
   } else {
     if (!attr[0]) { cudaFuncSetAttribute(phi_tiled_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr[0] = true; }
-    phi_tiled_kernel<false><<<grd, blk, sm, s>>>(kp, b, kz);
+    phi_tiled_kernel<false><<<grd, blk, sm, s>>>(tm, kp, b, kz);
   }
 }
 

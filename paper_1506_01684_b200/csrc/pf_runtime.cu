@@ -36,6 +36,9 @@ struct Block {
   double *phi[2][NPH];       // two copies (src/dst), allocation bases
   double *mu[2][NMU];
   int woff;                  // window offset (planes)
+  CUtensorMap tphi[2][NPH];  // TMA maps per time level: phi tile box,
+  CUtensorMap tmu[2][NMU];   //   mu tile box,
+  CUtensorMap tmui[2][NMU];  //   mu interior box
 };
 
 struct Plan {                // halo plan of one field in one copy
@@ -186,6 +189,51 @@ pf_status upload_ops(pf_ctx *c, const std::vector<CopyOp> &ops, CopyOp **d) {
   CK(cudaMalloc(d, ops.size() * sizeof(CopyOp)));
   CK(cudaMemcpy(*d, ops.data(), ops.size() * sizeof(CopyOp), cudaMemcpyHostToDevice));
   return PF_OK;
+}
+
+// TMA descriptor over a whole padded component allocation: dims {pitch,
+// ny+2, planes}, x fastest, FP64, box bx x by x 1, out-of-range boxes zero-filled.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+pf_status encode_map(pf_ctx *c, CUtensorMap *m, double *base, const Block &b, int bx, int by) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) return fail(c, PF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = (EncodeTiledFn)p;
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)b.pitch, (cuuint64_t)(b.ny + 2), (cuuint64_t)b.nplanes_alloc};
+  const cuuint64_t strides[2] = {(cuuint64_t)b.pitch * 8, (cuuint64_t)b.plane * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1}, es[3] = {1, 1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(c, PF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return PF_OK;
+}
+
+pf_status encode_maps(pf_ctx *c, Block &b) {
+  for (int cp = 0; cp < 2; ++cp) {
+    // tile boxes start one column left of the ring (16-byte aligned x): TILE_X + 4 wide
+    for (int a = 0; a < NPH; ++a) CKS(encode_map(c, &b.tphi[cp][a], b.phi[cp][a], b, TILE_X + 4, TILE_Y + 2));
+    for (int q = 0; q < NMU; ++q) {
+      CKS(encode_map(c, &b.tmu[cp][q], b.mu[cp][q], b, TILE_X + 4, TILE_Y + 2));
+      CKS(encode_map(c, &b.tmui[cp][q], b.mu[cp][q], b, TILE_X, TILE_Y));
+    }
+  }
+  return PF_OK;
+}
+
+TmaMaps maps_of(const pf_ctx *c, const Block &b) {
+  TmaMaps t;
+  const int s = c->cur, d = c->cur ^ 1;
+  for (int a = 0; a < NPH; ++a) { t.phi[a] = b.tphi[s][a]; t.phin[a] = b.tphi[d][a]; }
+  for (int q = 0; q < NMU; ++q) { t.mu[q] = b.tmu[s][q]; t.mui[q] = b.tmui[s][q]; }
+  return t;
 }
 
 // Build the halo plans of both fields and both copies.
@@ -359,6 +407,7 @@ BlockView view(const pf_ctx *c, const Block &b, int field_out) {
   else for (int q = 0; q < NMU; ++q) v.out[q] = b.mu[d][q] + o;
   v.nx = b.nx; v.ny = b.ny; v.nz = b.nz; v.pitch = b.pitch; v.plane = b.plane;
   v.tab = c->d_tab + (b.z0 + 1) * TAB;
+  v.zoff = 1 + b.woff;
   return v;
 }
 
@@ -663,6 +712,7 @@ pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
       }
     }
     c->blocks.push_back(b);
+    if (encode_maps(c, c->blocks.back()) != PF_OK) return bail(c->status);
   }
   // rank box
   {
@@ -803,7 +853,7 @@ pf_status pf_step(pf_ctx *c, int64_t n) {
       for (const auto &b : c->blocks) {
         const BlockView v = view(c, b, 0);
         if (c->p.variant == 1) launch_phi_naive(c->stream, c->kp, v);
-        else launch_phi_tiled(c->stream, c->kp, v);
+        else launch_phi_tiled(c->stream, c->kp, v, maps_of(c, b));
         c->launches++;
       }
     }
@@ -814,7 +864,7 @@ pf_status pf_step(pf_ctx *c, int64_t n) {
       for (const auto &b : c->blocks) {
         const BlockView v = view(c, b, 1);
         if (c->p.variant == 1) launch_mu_naive(c->stream, c->kp, v);
-        else launch_mu_tiled(c->stream, c->kp, v);
+        else launch_mu_tiled(c->stream, c->kp, v, maps_of(c, b));
         c->launches++;
       }
     }

@@ -13,7 +13,7 @@
 
 namespace pf {
 
-constexpr int TX = 32, TY = 8, RX = TX + 2, RY = TY + 2;
+constexpr int TX = TILE_X, TY = TILE_Y, RX = TX + 2, RY = TY + 2;
 constexpr int NTHR = TX * TY;
 constexpr int NRING = 2 * RX + 2 * TY;  // 84 ring cells incl. the 4 in-plane corners
 constexpr int NSLOT = 4;                // plane slots: k-1, k, k+1 in use, k+2 in flight
@@ -37,6 +37,58 @@ __device__ __forceinline__ void cp_async8(void *smem, const double *gmem, bool o
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// ---------------------------------------------------------------------------
+// TMA (cp.async.bulk.tensor) + mbarrier helpers.  One elected thread arms the
+// plane's mbarrier with the expected byte count and issues one bulk-tensor copy
+// per component box; every thread waits on the barrier's phase parity.
+// ---------------------------------------------------------------------------
+// A bulk-tensor box must start on a 16-byte boundary in x and land on a
+// 128-byte-aligned shared address (measured: tools/tma_probe.cu), so a staged
+// tile is RXS = TX + 4 doubles wide, starting one column left of the ring
+// (column i0 - 2, even because XO and i0 are): tile column c (c = 0 <-> i0 - 1)
+// lives at RXS-row offset c + 1.  TSZ pads the RY x RXS tile to 128 B.
+constexpr int RXS = TX + 4;
+constexpr int TSZ = ((RY * RXS * 8 + 127) / 128) * 128 / 8;
+static_assert(RY * RXS <= TSZ && (TSZ * 8) % 128 == 0, "tile padding");
+#define TILE_AT(arr, row, col) (arr)[(row) * RXS + (col) + 1]
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra.uni DONE;\n\t"
+      "bra.uni WAIT;\n"
+      "DONE:\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// 3D box (x fastest) of a tensor map into shared memory
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+// contiguous bytes (multiple of 16, 16-B aligned) into shared memory
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 
 // z-chunk length: enough CTAs to fill the 148 SMs several times over,
 // chunks of at least 16 planes.
