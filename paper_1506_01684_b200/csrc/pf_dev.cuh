@@ -29,6 +29,8 @@ struct KParams {
   double dt, inv_dt, inv_dx, inv_2dx, half_inv_dt;
   double dt_taueps[NPH];   // dt / (tau_a eps)
   double g2[6];            // 2 gamma_ab per pair
+  double gf4[6];           // 2 gamma_ab / (4 dx): isotropic face flux constant
+  double g2m[NPH][NPH];    // 2 gamma_ab as a matrix (0 on the diagonal)
   double delta[6];         // cubic anisotropy per pair
   double om[NPH][NPH];     // 16/pi^2 gamma_ab (0 on the diagonal)
   double g3[NPH];          // triple coefficient of the triple excluding x
@@ -94,22 +96,29 @@ __device__ __forceinline__ void pair_grad_aniso(double g2, double delta, const d
 __device__ __forceinline__ void phi_face(const KParams &kp, const double plo[NPH], const double phi_[NPH],
                                          const double glo[NPH][3], const double ghi[NPH][3], int d,
                                          double jf[NPH]) {
-  double pb[NPH], gn[NPH];
 #pragma unroll
-  for (int a = 0; a < NPH; ++a) {
-    pb[a] = RN_MUL(0.5, RN_ADD(plo[a], phi_[a]));
-    gn[a] = RN_MUL(RN_SUB(phi_[a], plo[a]), kp.inv_dx);
-    jf[a] = 0.0;
-  }
+  for (int a = 0; a < NPH; ++a) jf[a] = 0.0;
   if (!kp.aniso) {
+    // isotropic: with s = lo + hi = 2 phibar and t = hi - lo = dx grad_d phi,
+    // j_a = -sum_b 2 gamma_ab (phibar_a grad_b - phibar_b grad_a) phibar_b
+    //     = -sum_b [2 gamma_ab / (4 dx)] (s_a t_b - s_b t_a) s_b   (gf4 = 2 gamma / 4 dx)
+    double s[NPH], t[NPH];
+#pragma unroll
+    for (int a = 0; a < NPH; ++a) { s[a] = RN_ADD(plo[a], phi_[a]); t[a] = RN_SUB(phi_[a], plo[a]); }
 #pragma unroll
     for (int p = 0; p < 6; ++p) {
       const int a = pair_a(p), b = pair_b(p);
-      const double G = RN_MUL(kp.g2[p], RN_FMA(pb[a], gn[b], -RN_MUL(pb[b], gn[a])));
-      jf[a] = RN_FMA(-G, pb[b], jf[a]);
-      jf[b] = RN_FMA(G, pb[a], jf[b]);
+      const double G = RN_MUL(kp.gf4[p], RN_FMA(s[a], t[b], -RN_MUL(s[b], t[a])));
+      jf[a] = RN_FMA(-G, s[b], jf[a]);
+      jf[b] = RN_FMA(G, s[a], jf[b]);
     }
   } else {
+    double pb[NPH], gn[NPH];
+#pragma unroll
+    for (int a = 0; a < NPH; ++a) {
+      pb[a] = RN_MUL(0.5, RN_ADD(plo[a], phi_[a]));
+      gn[a] = RN_MUL(RN_SUB(phi_[a], plo[a]), kp.inv_dx);
+    }
     double gf[NPH][3];
 #pragma unroll
     for (int a = 0; a < NPH; ++a)
@@ -163,20 +172,45 @@ __device__ __forceinline__ void phi_cell_update_div(const KParams &kp, const dou
                                                     double out[NPH]) {
   // d a / d phi_a = sum_{b != a} g_ab(q_ab) . grad phi_b   (O4.2-4)
   double dad[NPH] = {0.0, 0.0, 0.0, 0.0};
+  if (!kp.aniso) {
+    // isotropic g = 2 gamma q: q_ab . grad_b = phi_a |grad_b|^2 - phi_b (grad_a . grad_b),
+    // so dad_a = sum_b 2 gamma_ab (phi_a G_bb - phi_b G_ab) with the Gram matrix G
+    double Gm[NPH][NPH];
 #pragma unroll
-  for (int p = 0; p < 6; ++p) {
-    const int a = pair_a(p), b = pair_b(p);
-    double q[3], g[3];
+    for (int a = 0; a < NPH; ++a)
 #pragma unroll
-    for (int e = 0; e < 3; ++e) q[e] = ph[a] * gc[b][e] - ph[b] * gc[a][e];
-    if (kp.aniso && kp.delta[p] != 0.0) {
-      pair_grad_aniso(kp.g2[p], kp.delta[p], q, g);
-    } else {
+      for (int b = a; b < NPH; ++b) {
+        Gm[a][b] = gc[a][0] * gc[b][0] + gc[a][1] * gc[b][1] + gc[a][2] * gc[b][2];
+        Gm[b][a] = Gm[a][b];
+      }
 #pragma unroll
-      for (int e = 0; e < 3; ++e) g[e] = kp.g2[p] * q[e];
+    for (int a = 0; a < NPH; ++a) {
+      double wd = 0.0, wo = 0.0;
+#pragma unroll
+      for (int b = 0; b < NPH; ++b) {
+        if (b == a) continue;
+        const double g2 = kp.g2m[a][b];
+        wd += g2 * Gm[b][b];
+        wo += g2 * (ph[b] * Gm[a][b]);
+      }
+      dad[a] = ph[a] * wd - wo;
     }
-    dad[a] += g[0] * gc[b][0] + g[1] * gc[b][1] + g[2] * gc[b][2];
-    dad[b] -= g[0] * gc[a][0] + g[1] * gc[a][1] + g[2] * gc[a][2];
+  } else {
+#pragma unroll
+    for (int p = 0; p < 6; ++p) {
+      const int a = pair_a(p), b = pair_b(p);
+      double q[3], g[3];
+#pragma unroll
+      for (int e = 0; e < 3; ++e) q[e] = ph[a] * gc[b][e] - ph[b] * gc[a][e];
+      if (kp.delta[p] != 0.0) {
+        pair_grad_aniso(kp.g2[p], kp.delta[p], q, g);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 3; ++e) g[e] = kp.g2[p] * q[e];
+      }
+      dad[a] += g[0] * gc[b][0] + g[1] * gc[b][1] + g[2] * gc[b][2];
+      dad[b] -= g[0] * gc[a][0] + g[1] * gc[a][1] + g[2] * gc[a][2];
+    }
   }
   // thermodynamics of the plane: psi_a = B_a - sum_c mu_c (mu_c/(4A) + chat)
   double ps[NPH];
@@ -227,7 +261,7 @@ __device__ __forceinline__ void phi_cell_update_div(const KParams &kp, const dou
   PF_CSWAP(u0, u1) PF_CSWAP(u2, u3) PF_CSWAP(u0, u2) PF_CSWAP(u1, u3) PF_CSWAP(u1, u2)
 #undef PF_CSWAP
   const double c1 = u0 - 1.0, c2 = c1 + u1, c3 = c2 + u2, c4 = c3 + u3;
-  const double t1 = c1, t2 = 0.5 * c2, t3 = c3 / 3.0, t4 = 0.25 * c4;
+  const double t1 = c1, t2 = 0.5 * c2, t3 = c3 * (1.0 / 3.0), t4 = 0.25 * c4;
   double theta = t1;
   if (u1 - t2 > 0.0) theta = t2;
   if (u2 - t3 > 0.0) theta = t3;
@@ -292,13 +326,14 @@ __device__ __forceinline__ void mu_face_t(const KParams &kp, const QL &lo, const
   for (int c = 0; c < NMU; ++c)
     out[c] = RN_MUL(RN_MUL(RN_MUL(0.5, RN_ADD(lo.M(c), hi.M(c))), RN_SUB(hi.mu(c), lo.mu(c))), kp.inv_dx);
   const double pbl = RN_MUL(0.5, RN_ADD(lo.pn(LIQ), hi.pn(LIQ)));
+  if (pbl == 0.0) return;                   // no liquid: J = 0 (bulk solid exits here)
   double gfl[3];
 #pragma unroll
   for (int e = 0; e < 3; ++e)
     gfl[e] = (e == d) ? RN_MUL(RN_SUB(hi.pn(LIQ), lo.pn(LIQ)), kp.inv_dx)
                       : RN_MUL(0.5, RN_ADD(lo.gt(LIQ, e), hi.gt(LIQ, e)));
   const double gl2 = RN_FMA(gfl[2], gfl[2], RN_FMA(gfl[1], gfl[1], RN_MUL(gfl[0], gfl[0])));
-  if (pbl == 0.0 || gl2 == 0.0) return;     // no liquid / flat liquid: J = 0
+  if (gl2 == 0.0) return;                   // flat liquid: J = 0
   double pb[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) pb[a] = RN_MUL(0.5, RN_ADD(lo.pn(a), hi.pn(a)));
@@ -354,26 +389,32 @@ __device__ __forceinline__ void mu_cell_update(const KParams &kp, const double *
                                                const double divf[NMU], double out[NMU]) {
   const double So = po[0] * po[0] + po[1] * po[1] + po[2] * po[2] + po[3] * po[3];
   const double Sn = pn[0] * pn[0] + pn[1] * pn[1] + pn[2] * pn[2] + pn[3] * pn[3];
-  const double rSo = 1.0 / So, rSn = 1.0 / Sn;
+  // one reciprocal for both 1/S (S in [1/4, 1] on the simplex)
+  const double rS = 1.0 / (So * Sn), rSo = Sn * rS, rSn = So * rS;
   double hn[NPH], dh[NPH];
 #pragma unroll
   for (int a = 0; a < NPH; ++a) {
     hn[a] = pn[a] * pn[a] * rSn;
     dh[a] = hn[a] - po[a] * po[a] * rSo;
   }
+  double chi[NMU], rest[NMU];
 #pragma unroll
   for (int c = 0; c < NMU; ++c) {
-    double chi = 0.0, s = 0.0, dcdT = 0.0;
+    double x = 0.0, s = 0.0, dcdT = 0.0;
 #pragma unroll
     for (int a = 0; a < NPH; ++a) {
       const double i2a = tab[T_INV2A + a * 2 + c];
-      chi += hn[a] * i2a;                                                  // O5.3
+      x += hn[a] * i2a;                                                    // O5.3
       s += (mu[c] * i2a + tab[T_CHAT + a * 2 + c]) * dh[a];                // O5.4 (sign below)
       dcdT += hn[a] * (tab[T_MCHAT + a * 2 + c] - mu[c] * tab[T_KAPPA + a * 2 + c]);  // O5.5
     }
-    // mu^{n+1} = mu + dt/chi [ -s/dt + dcdT G v + div ]
-    out[c] = mu[c] + kp.dt / chi * (dcdT * kp.Gv - s * kp.inv_dt + divf[c] * kp.inv_dx);
+    chi[c] = x;
+    rest[c] = dcdT * kp.Gv - s * kp.inv_dt + divf[c] * kp.inv_dx;
   }
+  // mu^{n+1} = mu + dt/chi [ -s/dt + dcdT G v + div ]; one reciprocal for both chi
+  const double rc = kp.dt / (chi[0] * chi[1]);
+  out[0] = mu[0] + (chi[1] * rc) * rest[0];
+  out[1] = mu[1] + (chi[0] * rc) * rest[1];
 }
 
 }  // namespace pf

@@ -177,6 +177,8 @@ __global__ void __launch_bounds__(NTHR, 2) mu_tiled_kernel(const __grid_constant
       }
     }
     __syncthreads();  // C: M of plane k visible; faces of plane k-1 consumed
+    // phi^{n+1}(k+1), staged at A(k-1), first needed now
+    if (k > k0) mbar_wait(&S.bar_pn[slot(k + 1)], par4(k + 1));
     // D: faces of plane k
     {
       double f[NMU];
@@ -219,7 +221,6 @@ __global__ void __launch_bounds__(NTHR, 2) mu_tiled_kernel(const __grid_constant
       for (int a = 0; a < NPH; ++a) pn_c[a] = T(S.pn[sn][a], orow, oc);
     }
     __syncthreads();  // E
-    if (k + 2 <= k1) mbar_wait(&S.bar_pn[slot(k + 2)], par4(k + 2));  // for the next iteration
     // F: cell update of (i, j, k)
     if (active) {
       double divf[NMU], out[NMU];
