@@ -42,13 +42,6 @@ def _env_int(k, d):
         return d
 
 
-def flops_per_lup():
-    from oracle import oracle as O
-    from inputs import gen
-    pd = gen.load_params("v1")
-    return O.count_flops(O.make_params(pd, layer_height=64))
-
-
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
     FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
@@ -101,29 +94,69 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_oracle_sample(steps: int, nz_slab: int = 16):
+def load_cfg(name):
+    return json.load(open(os.path.join(ROOT, "configs", f"{name}.json")))
+
+
+def workload(name: str, world: int):
+    """Global grid, block grid and per-rank cells of a config at `world` ranks:
+    weak scaling (per-GPU block, C4) or strong scaling (fixed global grid, C5)."""
+    from paper_1506_01684_b200 import dist as pdist
+    cfg = load_cfg(name)
+    if cfg.get("per_gpu"):
+        (NX, NY, NZ), blocks = pdist.weak_grid(world, per=cfg["nx"], config=name)
+        scaling = "weak"
+    else:
+        NX, NY, NZ = cfg["nx"], cfg["ny"], cfg["nz"]
+        blocks = pdist.decomposition(world, name)
+        scaling = "strong"
+    return cfg, (NX, NY, NZ), blocks, NX * NY * NZ // world, scaling
+
+
+def flops_per_lup(cfg):
+    from oracle import oracle as O
+    from inputs import gen
+    pd = gen.load_params("v1")
+    return O.count_flops(O.make_params(pd, layer_height=cfg["init"]["layer_height"], aniso=cfg.get("aniso", False),
+                                       delta_sl=cfg.get("delta_sl")))
+
+
+def cpu_oracle_sample(name: str, steps: int, nz_slab: int = 16):
     """Time the CPU oracle (as it stands) on a bounded sample of the workload:
-    the 512 x 512 x nz_slab slab of the C4 initial state that contains the
-    solid-liquid front, stepped as its own domain (uniform per-cell work: the
-    oracle takes no shortcuts).  Returns (MLUP/s, cores, sample text)."""
+    the full x-y extent of one GPU's block, nz_slab planes around the
+    solid-liquid front of the config's initial state, stepped as its own domain
+    (uniform per-cell work: the oracle takes no shortcuts).
+    Returns (MLUP/s, cores, sample text)."""
     from inputs import gen
     from oracle import oracle as O
-    cfg = json.load(open(os.path.join(ROOT, "configs", f"{CONFIG}.json")))
+    cfg = load_cfg(name)
     pd = gen.load_params("v1")
     lh = cfg["init"]["layer_height"]
-    spec = gen.spec_from_config(cfg, 512, 512)
+    nx, ny = min(cfg["nx"], 512), min(cfg["ny"], 512)
+    spec = gen.spec_from_config(cfg, cfg["nx"], cfg["ny"])
     z0 = int(lh) - nz_slab // 2
-    phi, mu = gen.generate(spec, 512, 512, 512, box=(0, 0, z0, 512, 512, nz_slab))
-    p = O.make_params(pd, layer_height=lh - z0)
+    phi, mu = gen.generate(spec, cfg["nx"], cfg["ny"], cfg["nz"], box=(0, 0, z0, nx, ny, nz_slab))
+    p = O.make_params(pd, layer_height=lh - z0, aniso=cfg.get("aniso", False), delta_sl=cfg.get("delta_sl"))
     t0 = time.perf_counter()
     for s in range(steps):
         phi, mu = O.step(p, phi, mu, s, 0)
     dt = time.perf_counter() - t0
-    cells = 512 * 512 * nz_slab
+    cells = nx * ny * nz_slab
     cores = _env_int("OMP_NUM_THREADS", os.cpu_count() or 1)
     return cells * steps / dt / 1e6, cores, \
-        f"{steps} oracle step(s) of the 512x512x{nz_slab} slab z in [{z0},{z0 + nz_slab}) of the C4 state " \
-        f"({cells * steps} LUP, {dt:.1f} s)"
+        f"{steps} oracle step(s) of the {nx}x{ny}x{nz_slab} slab z in [{z0},{z0 + nz_slab}) of the " \
+        f"{cfg['name']} state ({cells * steps} LUP, {dt:.1f} s)"
+
+
+def describe(cfg, grid, blocks, scaling):
+    NX, NY, NZ = grid
+    px, py, pz = blocks
+    kind = "anisotropic (cubic, delta_sl = %g)" % cfg["delta_sl"] if cfg.get("aniso") else "isotropic"
+    per = f"{cfg['nx']}^3 cells per GPU (weak scaling)" if scaling == "weak" else \
+        f"{NX}x{NY}x{NZ} cells total (strong scaling)"
+    return (f"{cfg['name']}: {per}, FP64, N=4 phases, K=3 components, periodic x/y, zero-flux z, "
+            f"{cfg['init']['kind']} solid layer z<{cfg['init']['layer_height']}, mu noise "
+            f"{cfg['init'].get('mu_noise', 0)}, {kind}" + (", moving window" if cfg.get("window") else ""))
 
 
 def run_reference(args):
@@ -131,15 +164,17 @@ def run_reference(args):
     if rank != 0:
         return 0
     steps, warm = args.steps, args.warmup
-    from oracle import oracle as O  # noqa: F401  (builds the oracle)
+    world = _env_int("WORLD_SIZE", 1)
+    cfg, grid, blocks, cells_local, scaling = workload(args.config, world)
     # each step: one oracle step over a bounded sample of the workload
-    _ = cpu_oracle_sample(max(0, min(warm, 1)), nz_slab=16) if warm else None
-    v, cores, sample = cpu_oracle_sample(steps, nz_slab=16)
+    if warm:
+        cpu_oracle_sample(args.config, 1, nz_slab=16)
+    v, cores, sample = cpu_oracle_sample(args.config, steps, nz_slab=16)
     line = {"impl": "reference", "metric": "MLUP/s", "value": round(v, 3), "unit": "MLUP/s",
-            "n_gpus": args.gpus, "steps": steps, "warmup": warm, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C4 512^3 per GPU, Voronoi solid layer z<64, PARAMS-v1 (CPU oracle on a "
-                                   "bounded slab sample)", "global_cells_per_gpu": 512 ** 3},
+            "n_gpus": world, "steps": steps, "warmup": warm, "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": describe(cfg, grid, blocks, scaling) + " — CPU oracle on a bounded slab sample",
+                       "global_cells": cells_local * world},
             "cpu_baseline": {"value": round(v, 3), "unit": "MLUP/s", "cores": cores, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": round(v, 3), "unit": "MLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -154,14 +189,12 @@ def run_gpu(args):
     from paper_1506_01684_b200 import dist as pdist
 
     rank, world, local = pdist.env_rank()
-    n = args.gpus if world == 1 else world
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
-    cfg = json.load(open(os.path.join(ROOT, "configs", f"{CONFIG}.json")))
-    (NX, NY, NZ), (px, py, pz) = pdist.weak_grid(world if world > 1 else 1, per=512, config=CONFIG)
+    cfg, (NX, NY, NZ), (px, py, pz), cells_local, scaling = workload(args.config, world)
     from inputs import gen
     pd = gen.load_params("v1")
     prm = pf.make_params(pd, cfg, nx=NX, ny=NY, nan_check_every=0)
@@ -170,7 +203,7 @@ def run_gpu(args):
     ctx = pf.Context(NX, NY, NZ, prm, px, py, pz, rank=rank if world > 1 else 0, nranks=world,
                      device=local if world > 1 else 0, nccl_id=nid, stream=stream.cuda_stream)
     ctx.init(cfg["seed"])
-    cells_local = 512 ** 3
+    shape = ctx.shape
 
     def barrier():
         if world > 1:
@@ -206,24 +239,27 @@ def run_gpu(args):
 
     # end-to-end through the C ABI with host buffers: each step writes the
     # state from pinned host memory, advances one step, reads it back
-    e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    hphi = torch.empty((4, 512, 512, 512), dtype=torch.float64, pin_memory=True)
-    hmu = torch.empty((2, 512, 512, 512), dtype=torch.float64, pin_memory=True)
-    ctx.read(hphi, hmu)
-    barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        ctx.write(hphi, hmu)
-        ctx.step(1)
-        ctx.read(hphi, hmu)
-    barrier()
-    e2e_s = max_over_ranks(time.perf_counter() - t0)
-    e2e = cells_local * world * e2e_steps / e2e_s / 1e6
+    e2e = None
     state_bytes = cells_local * 6 * 8
+    e2e_steps = min(args.steps, args.e2e_steps)
+    if e2e_steps > 0:
+        hphi = torch.empty((4,) + shape, dtype=torch.float64, pin_memory=True)
+        hmu = torch.empty((2,) + shape, dtype=torch.float64, pin_memory=True)
+        ctx.read(hphi, hmu)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            ctx.write(hphi, hmu)
+            ctx.step(1)
+            ctx.read(hphi, hmu)
+        barrier()
+        e2e_s = max_over_ranks(time.perf_counter() - t0)
+        e2e = cells_local * world * e2e_steps / e2e_s / 1e6
+        del hphi, hmu
 
     if rank == 0:
-        fl = flops_per_lup()
+        fl = flops_per_lup(cfg)
         peaks = {}
         try:
             peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -244,23 +280,23 @@ def run_gpu(args):
         traffic = None
         try:
             prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-            traffic = prof.get("dram_bytes_per_launch", {}).get(dom)
+            if prof.get("config", "c4") == args.config:
+                traffic = prof.get("dram_bytes_per_launch", {}).get(dom)
         except (OSError, ValueError):
             pass
         cpu_v, cores, sample = (None, None, "skipped")
         if world == 1 and not args.no_cpu:
-            cpu_v, cores, sample = cpu_oracle_sample(args.cpu_steps, nz_slab=64)
+            cpu_v, cores, sample = cpu_oracle_sample(args.config, args.cpu_steps,
+                                                     nz_slab=64 if not cfg.get("aniso") else 16)
         line = {
             "metric": "MLUP/s", "value": round(value, 2), "unit": "MLUP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded Voronoi solid layer, PARAMS-v1)",
-            "config": {"workload": "C4: 512^3 cells per GPU (weak scaling), FP64, N=4 phases, K=3 components, "
-                                   "periodic x/y, zero-flux z, Voronoi solid layer z<64 (~1 seed per 32x32), "
-                                   "mu noise 1e-3, isotropic",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded initial state, PARAMS-v1)",
+            "config": {"workload": describe(cfg, (NX, NY, NZ), (px, py, pz), scaling),
                        "global_cells": cells_local * world, "grid": [NX, NY, NZ], "blocks": [px, py, pz],
                        "parallelism": f"block{px}x{py}x{pz}",
-                       "l2": "inputs larger than L2 (12.9 GB of fields per GPU vs 126 MB L2)"},
+                       "l2": f"inputs larger than L2 ({cells_local * 96 / 1e9:.1f} GB of fields per GPU vs 126 MB L2)"},
             "roofline": {"bound": "alu", "kernel": f"{dom}-sweep", "achieved": round(d["tflops"], 3),
                          "peak": round(PEAK_FP64_DERIVED, 2), "unit": "TFLOP/s",
                          "frac": round(d["frac_fp64"], 4), "traffic": traffic,
@@ -271,8 +307,9 @@ def run_gpu(args):
                          "hbm_peak_gbs": hbm},
             "cpu_baseline": {"value": round(cpu_v, 3) if cpu_v else None, "unit": "MLUP/s", "cores": cores,
                              "kind": "oracle", "sample": sample},
-            "e2e": {"value": round(e2e, 2), "unit": "MLUP/s", "h2d_bytes_per_step": state_bytes,
-                    "d2h_bytes_per_step": state_bytes, "steps": e2e_steps,
+            "e2e": {"value": round(e2e, 2) if e2e else None, "unit": "MLUP/s",
+                    "h2d_bytes_per_step": state_bytes if e2e else 0,
+                    "d2h_bytes_per_step": state_bytes if e2e else 0, "steps": e2e_steps,
                     "what": "pf_write(pinned host state) + pf_step(1) + pf_read(pinned host) per step"},
             "gpu_launches": launches,
             "clocks": clk,
@@ -293,6 +330,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-steps", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--config", default=CONFIG, choices=["c4", "c5"],
+                    help="c4: weak scaling 512^3 per GPU (default, the headline); c5: strong scaling 1024^3, anisotropic")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

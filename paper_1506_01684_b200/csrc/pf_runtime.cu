@@ -543,23 +543,25 @@ pf_status move_state(pf_ctx *c, double *phi, double *mu, bool to_fields) {
     double *user = field == 0 ? phi : mu;
     const int ncomp = field == 0 ? NPH : NMU;
     const bool dev = is_device_ptr(user);
-    double *buf = dev ? user : c->d_stage;
-    if (to_fields && !dev)
-      CK(cudaMemcpyAsync(buf, user, (size_t)n * ncomp * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    for (const auto &b : c->blocks) {
-      const double *f[NPH];
-      double *w[NPH];
-      for (int q = 0; q < ncomp; ++q) {
-        double *base = field_ptr(b, field, c->cur, q) + cell_off(b, 0, 0, 0);
-        f[q] = base;
-        w[q] = base;
-      }
-      launch_gather(c->stream, f, ncomp, b.nx, b.ny, b.nz, b.pitch, b.plane, buf, c->box_nx, c->box_ny, n,
-                    b.x0 - c->box_x0, b.y0 - c->box_y0, b.z0 - c->box_z0, to_fields, w);
+    if (!dev && !c->d_stage) {  // one component of staging, allocated on first host transfer
+      c->stage_elems = n;
+      CK(cudaMalloc(&c->d_stage, (size_t)n * sizeof(double)));
     }
-    CK(cudaGetLastError());
-    if (!to_fields && !dev)
-      CK(cudaMemcpyAsync(user, buf, (size_t)n * ncomp * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    for (int q = 0; q < ncomp; ++q) {  // component by component (bounded staging)
+      double *buf = dev ? user + (int64_t)q * n : c->d_stage;
+      if (to_fields && !dev)
+        CK(cudaMemcpyAsync(buf, user + (int64_t)q * n, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      for (const auto &b : c->blocks) {
+        double *base = field_ptr(b, field, c->cur, q) + cell_off(b, 0, 0, 0);
+        const double *f[NPH] = {base, nullptr, nullptr, nullptr};
+        double *w[NPH] = {base, nullptr, nullptr, nullptr};
+        launch_gather(c->stream, f, 1, b.nx, b.ny, b.nz, b.pitch, b.plane, buf, c->box_nx, c->box_ny, n,
+                      b.x0 - c->box_x0, b.y0 - c->box_y0, b.z0 - c->box_z0, to_fields, w);
+      }
+      CK(cudaGetLastError());
+      if (!to_fields && !dev)
+        CK(cudaMemcpyAsync(user + (int64_t)q * n, buf, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    }
   }
   CK(cudaStreamSynchronize(c->stream));
   return PF_OK;
@@ -735,10 +737,6 @@ pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
   if (cudaMalloc(&c->d_tab, (size_t)c->tab_planes * TAB * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&c->d_red, 4 * sizeof(unsigned long long)) != cudaSuccess) {
     fail(c, PF_ERR_CUDA, "alloc table"); return bail(PF_ERR_CUDA);
-  }
-  c->stage_elems = c->box_nx * c->box_ny * c->box_nz * NPH;
-  if (cudaMalloc(&c->d_stage, (size_t)c->stage_elems * sizeof(double)) != cudaSuccess) {
-    cudaGetLastError(); fail(c, PF_ERR_CUDA, "alloc staging"); return bail(PF_ERR_CUDA);
   }
   if (g->nranks > 1) {
     ncclUniqueId id;

@@ -240,7 +240,7 @@ def test_c2_full_one_step(pv1):
     assert O.rel_maxnorm(gmu, omu) <= TOL1
 
 
-@pytest.mark.parametrize("name,shape", [("c4", (512, 512, 512)), ("c3", (256, 256, 1024))])
+@pytest.mark.parametrize("name,shape", [("c4", (512, 512, 512)), ("c3", (256, 256, 1024)), ("c5", (1024, 1024, 256))])
 def test_full_size_sampled_one_step(pv1, name, shape):
     nx, ny, nz = shape
     cfg, (phi, mu) = _state(name, nx, ny, nz)
