@@ -9,7 +9,9 @@
 namespace pf {
 
 constexpr int XO = 4;  // column of interior i = 0 within a padded row (i = -1 at 3)
-constexpr int TILE_X = 32, TILE_Y = 8;  // CTA tile of the z-marching sweeps (pf_tile.cuh)
+// CTA tiles of the z-marching sweeps (pf_tile.cuh): 32 x 4 for the phi-sweep
+// (4 CTAs / SM), 32 x 8 for the mu-sweep (2 CTAs / SM) — measured best.
+constexpr int TILE_X = 32, PHI_TILE_Y = 4, MU_TILE_Y = 8;
 
 // TMA descriptors of one block's fields in one time level (encoded on the host
 // over the whole padded allocation: dims {pitch, ny+2, planes}, x fastest).

@@ -16,6 +16,8 @@
 // in registers; the own column's phi^n / mu at k+1 (the z-face's upper cell)
 // come from registers.  All arithmetic is the pinned code of pf_dev.cuh, so
 // results do not depend on tile or block boundaries.
+#include "pf_kernels.cuh"
+#define PF_TILE_Y MU_TILE_Y
 #include "pf_tile.cuh"
 
 namespace pf {
@@ -55,7 +57,7 @@ struct RawQ {
   __device__ __forceinline__ double dcl(int a, int c) const { return dcl_of(tab, a, c, mu(c)); }
 };
 
-__global__ void __launch_bounds__(NTHR, 2) mu_tiled_kernel(const __grid_constant__ TmaMaps tm, KParams kp,
+__global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid_constant__ TmaMaps tm, KParams kp,
                                                            BlockView b, int kz) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   MuSmem &S = *reinterpret_cast<MuSmem *>(smem_raw);

@@ -12,6 +12,8 @@
 // slots guarded by mbarriers.  Two CTA barriers per plane.  The face and
 // gradient routines are the pinned ones of pf_dev.cuh: a face evaluated at a
 // tile / chunk / block edge has the same bits as mid-tile.
+#include "pf_kernels.cuh"
+#define PF_TILE_Y PHI_TILE_Y
 #include "pf_tile.cuh"
 
 namespace pf {
@@ -28,7 +30,7 @@ struct __align__(128) PhiSmem {
 constexpr uint32_t PHI_STAGE_BYTES = (NPH * RXS * RY + NMU * TX * TY + TAB) * 8;
 
 template <bool ANISO>
-__global__ void __launch_bounds__(NTHR, 2) phi_tiled_kernel(const __grid_constant__ TmaMaps tm, KParams kp, BlockView b,
+__global__ void __launch_bounds__(NTHR, 512 / NTHR) phi_tiled_kernel(const __grid_constant__ TmaMaps tm, KParams kp, BlockView b,
                                                             int kz) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   PhiSmem &S = *reinterpret_cast<PhiSmem *>(smem_raw);

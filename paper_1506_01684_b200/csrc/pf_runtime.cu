@@ -36,9 +36,10 @@ struct Block {
   double *phi[2][NPH];       // two copies (src/dst), allocation bases
   double *mu[2][NMU];
   int woff;                  // window offset (planes)
-  CUtensorMap tphi[2][NPH];  // TMA maps per time level: phi tile box,
-  CUtensorMap tmu[2][NMU];   //   mu tile box,
-  CUtensorMap tmui[2][NMU];  //   mu interior box
+  CUtensorMap tphi[2][NPH];  // TMA maps per time level: phi tile box (phi-sweep tile),
+  CUtensorMap tphim[2][NPH]; //   phi tile box (mu-sweep tile),
+  CUtensorMap tmu[2][NMU];   //   mu tile box (mu-sweep tile),
+  CUtensorMap tmui[2][NMU];  //   mu interior box (phi-sweep tile)
 };
 
 struct Plan {                // halo plan of one field in one copy
@@ -218,20 +219,29 @@ pf_status encode_map(pf_ctx *c, CUtensorMap *m, double *base, const Block &b, in
 
 pf_status encode_maps(pf_ctx *c, Block &b) {
   for (int cp = 0; cp < 2; ++cp) {
-    // tile boxes start one column left of the ring (16-byte aligned x): TILE_X + 4 wide
-    for (int a = 0; a < NPH; ++a) CKS(encode_map(c, &b.tphi[cp][a], b.phi[cp][a], b, TILE_X + 4, TILE_Y + 2));
+    // tile boxes start one column left of the ring (16-byte aligned x): TILE_X + 4 wide;
+    // phi-sweep tiles are PHI_TILE_Y high, mu-sweep tiles MU_TILE_Y
+    for (int a = 0; a < NPH; ++a) {
+      CKS(encode_map(c, &b.tphi[cp][a], b.phi[cp][a], b, TILE_X + 4, PHI_TILE_Y + 2));
+      CKS(encode_map(c, &b.tphim[cp][a], b.phi[cp][a], b, TILE_X + 4, MU_TILE_Y + 2));
+    }
     for (int q = 0; q < NMU; ++q) {
-      CKS(encode_map(c, &b.tmu[cp][q], b.mu[cp][q], b, TILE_X + 4, TILE_Y + 2));
-      CKS(encode_map(c, &b.tmui[cp][q], b.mu[cp][q], b, TILE_X, TILE_Y));
+      CKS(encode_map(c, &b.tmu[cp][q], b.mu[cp][q], b, TILE_X + 4, MU_TILE_Y + 2));
+      CKS(encode_map(c, &b.tmui[cp][q], b.mu[cp][q], b, TILE_X, PHI_TILE_Y));
     }
   }
   return PF_OK;
 }
 
-TmaMaps maps_of(const pf_ctx *c, const Block &b) {
+// descriptors of the current time levels for the phi-sweep (field 0) or the
+// mu-sweep (field 1)
+TmaMaps maps_of(const pf_ctx *c, const Block &b, int field) {
   TmaMaps t;
   const int s = c->cur, d = c->cur ^ 1;
-  for (int a = 0; a < NPH; ++a) { t.phi[a] = b.tphi[s][a]; t.phin[a] = b.tphi[d][a]; }
+  for (int a = 0; a < NPH; ++a) {
+    t.phi[a] = field == 0 ? b.tphi[s][a] : b.tphim[s][a];
+    t.phin[a] = b.tphim[d][a];
+  }
   for (int q = 0; q < NMU; ++q) { t.mu[q] = b.tmu[s][q]; t.mui[q] = b.tmui[s][q]; }
   return t;
 }
@@ -853,7 +863,7 @@ pf_status pf_step(pf_ctx *c, int64_t n) {
       for (const auto &b : c->blocks) {
         const BlockView v = view(c, b, 0);
         if (c->p.variant == 1) launch_phi_naive(c->stream, c->kp, v);
-        else launch_phi_tiled(c->stream, c->kp, v, maps_of(c, b));
+        else launch_phi_tiled(c->stream, c->kp, v, maps_of(c, b, 0));
         c->launches++;
       }
     }
@@ -864,7 +874,7 @@ pf_status pf_step(pf_ctx *c, int64_t n) {
       for (const auto &b : c->blocks) {
         const BlockView v = view(c, b, 1);
         if (c->p.variant == 1) launch_mu_naive(c->stream, c->kp, v);
-        else launch_mu_tiled(c->stream, c->kp, v, maps_of(c, b));
+        else launch_mu_tiled(c->stream, c->kp, v, maps_of(c, b, 1));
         c->launches++;
       }
     }
