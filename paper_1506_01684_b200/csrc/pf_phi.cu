@@ -22,8 +22,8 @@ struct __align__(128) PhiSmem {
   double p[NSLOT][NPH][TSZ];       // phi^n tile planes, (row, col) at row * RX + col
   double mu[NSLOT][NMU][TY * TX];  // mu^n of the interior cells
   double tab[NSLOT][TAB];          // per-plane table rows
-  double fx[NPH][TY][TX + 1];      // x-face fluxes at i - 1/2, i = 0..TX
-  double fy[NPH][TY + 1][TX];      // y-face fluxes at j - 1/2, j = 0..TY
+  double fx[1][NPH][TY][TX + 1];   // x-face fluxes at i - 1/2, i = 0..TX
+  double fy[1][NPH][TY + 1][TX];   // y-face fluxes at j - 1/2, j = 0..TY
   uint64_t bar[NSLOT];             // one mbarrier per slot
 };
 
@@ -100,12 +100,17 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) phi_tiled_kernel(const __gri
     phi_face(kp, lo, hi, ANISO ? gl : gdum, ANISO ? gh : gdum, 2, jzm);
   }
 
+  // Two CTA barriers per plane: C (faces of plane k-1 consumed) and B (faces of
+  // plane k complete).  A single barrier with plane-parity face buffers was
+  // measured slower: the second buffer costs a CTA per SM of occupancy.
+  // TMA refills slot(k+2) = slot(k-2), last read in D(k-1), before B(k-1).
   for (int k = k0; k < k1; ++k) {
     // A: stage plane k+2 (needed from iteration k+1 on); wait for plane k+1
     if (tid == 0 && k + 2 <= k1) stage(k + 2);
     wait(k + 1);
-    __syncthreads();  // C: faces of plane k-1 consumed by everybody
+    __syncthreads();  // C
     const int sc = slot(k), sm = slot(k - 1), sp = slot(k + 1);
+    const int fb = 0;
     // D: faces of plane k; own column values to registers
     double pm[NPH], pc[NPH], pp[NPH], jzp[NPH];
     {
@@ -122,8 +127,8 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) phi_tiled_kernel(const __gri
         phi_face(kp, lo, hi, ANISO ? gl : gdum, ANISO ? gh : gdum, d, jf);
 #pragma unroll
         for (int a = 0; a < NPH; ++a) {
-          if (d == 0) S.fx[a][ty][tx] = jf[a];
-          else S.fy[a][ty][tx] = jf[a];
+          if (d == 0) S.fx[fb][a][ty][tx] = jf[a];
+          else S.fy[fb][a][ty][tx] = jf[a];
         }
       }
       // far faces: +y of the last row (warp 0), +x of the last column (warp 1)
@@ -140,8 +145,8 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) phi_tiled_kernel(const __gri
         phi_face(kp, lo, hi, ANISO ? gl : gdum, ANISO ? gh : gdum, d, jf);
 #pragma unroll
         for (int a = 0; a < NPH; ++a) {
-          if (d == 0) S.fx[a][r0 - 1][TX] = jf[a];
-          else S.fy[a][TY][c0 - 1] = jf[a];
+          if (d == 0) S.fx[fb][a][r0 - 1][TX] = jf[a];
+          else S.fy[fb][a][TY][c0 - 1] = jf[a];
         }
       }
       // z-face k+1/2 (own column)
@@ -157,7 +162,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) phi_tiled_kernel(const __gri
       }
       phi_face(kp, pc, pp, ANISO ? gl : gdum, ANISO ? gh : gdum, 2, jzp);
     }
-    __syncthreads();  // E
+    __syncthreads();  // B: faces of plane k complete
     // F: cell update of (i, j, k)
     if (active) {
       double gc[NPH][3], dsum[NPH], mu[NMU], out[NPH];
@@ -166,7 +171,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) phi_tiled_kernel(const __gri
         gc[a][0] = cgrad(kp, T(S.p[sc][a], orow, oc - 1), T(S.p[sc][a], orow, oc + 1));
         gc[a][1] = cgrad(kp, T(S.p[sc][a], orow - 1, oc), T(S.p[sc][a], orow + 1, oc));
         gc[a][2] = cgrad(kp, pm[a], pp[a]);
-        dsum[a] = ((S.fx[a][ty][tx + 1] - S.fx[a][ty][tx]) + (S.fy[a][ty + 1][tx] - S.fy[a][ty][tx])) +
+        dsum[a] = ((S.fx[fb][a][ty][tx + 1] - S.fx[fb][a][ty][tx]) + (S.fy[fb][a][ty + 1][tx] - S.fy[fb][a][ty][tx])) +
                   (jzp[a] - jzm[a]);
       }
       mu[0] = S.mu[sc][0][ty * TX + tx];
