@@ -92,7 +92,12 @@ typedef struct {
   /* initial condition recipe for pf_init */
   int32_t init_kind;          /* 0 voronoi, 1 lamellar, 2 planar                   */
   int32_t init_n_seeds;
-  int32_t init_lam_wmin, init_lam_wmax, init_planar_phase, pad_;
+  int32_t init_lam_wmin, init_lam_wmax, init_planar_phase;
+  int32_t shortcuts;          /* 1: region shortcuts —
+                                 a warp of bulk cells (pure phase, identical D3C7
+                                 (D3C19 if aniso) neighbourhood) skips the phi
+                                 update, whose result is then its input bit for
+                                 bit; results identical to shortcuts = 0         */
   double init_layer_height, init_iface_width, init_mu_noise;
 } pf_params;
 

@@ -37,7 +37,21 @@ struct KParams {
   double pi_eps_4;         // pi eps / 4
   double Gv;               // G v = -dT/dt
   int aniso;
+  int shortcuts;           // region shortcuts (NEXT-1): skip the phi update of bulk warps
 };
+
+// A cell whose phase vector is a simplex vertex (one component exactly 1, the
+// others exactly 0).  With an identical neighbourhood its phi update returns
+// it unchanged bit for bit: every gradient and face flux is exactly 0, the
+// driving force vanishes (S = 1, psi-bar = psi_p), and the projection maps
+// 1 + dt/(tau eps) mean back to exactly 1 (Sterbenz) and the pushed-down
+// absent phases to exactly 0 — so skipping it is exact.
+__device__ __forceinline__ bool is_vertex(const double p[NPH]) {
+  int ones = 0, zeros = 0;
+#pragma unroll
+  for (int a = 0; a < NPH; ++a) { ones += p[a] == 1.0; zeros += p[a] == 0.0; }
+  return ones == 1 && zeros == NPH - 1;
+}
 
 // Per-plane table (T-only subexpressions once per
 // x-y slice).  TAB doubles per plane, index = global window plane + 1.

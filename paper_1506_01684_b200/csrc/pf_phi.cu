@@ -163,8 +163,32 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) phi_tiled_kernel(const __gri
       phi_face(kp, pc, pp, ANISO ? gl : gdum, ANISO ? gh : gdum, 2, jzp);
     }
     __syncthreads();  // B: faces of plane k complete
-    // F: cell update of (i, j, k)
-    if (active) {
+    // region shortcut (NEXT-1): a warp whose cells
+    // are all simplex vertices with an identical D3C7 (D3C19) neighbourhood
+    // keeps phi^{n+1} = phi^n — bitwise what the full update returns (is_vertex)
+    bool skip = false;
+    if (kp.shortcuts) {
+      bool mine = is_vertex(pc);
+#pragma unroll
+      for (int a = 0; a < NPH; ++a) {
+        const double v = pc[a];
+        mine = mine && T(S.p[sc][a], orow, oc - 1) == v && T(S.p[sc][a], orow, oc + 1) == v &&
+               T(S.p[sc][a], orow - 1, oc) == v && T(S.p[sc][a], orow + 1, oc) == v && pm[a] == v && pp[a] == v;
+        if (ANISO)
+          mine = mine && T(S.p[sc][a], orow - 1, oc - 1) == v && T(S.p[sc][a], orow - 1, oc + 1) == v &&
+                 T(S.p[sc][a], orow + 1, oc - 1) == v && T(S.p[sc][a], orow + 1, oc + 1) == v &&
+                 T(S.p[sm][a], orow, oc - 1) == v && T(S.p[sm][a], orow, oc + 1) == v &&
+                 T(S.p[sm][a], orow - 1, oc) == v && T(S.p[sm][a], orow + 1, oc) == v &&
+                 T(S.p[sp][a], orow, oc - 1) == v && T(S.p[sp][a], orow, oc + 1) == v &&
+                 T(S.p[sp][a], orow - 1, oc) == v && T(S.p[sp][a], orow + 1, oc) == v;
+      }
+      skip = __all_sync(0xffffffffu, mine || !active);
+    }
+    if (active && skip) {
+      const int64_t o = (int64_t)k * b.plane + colo;
+#pragma unroll
+      for (int a = 0; a < NPH; ++a) b.out[a][o] = pc[a];
+    } else if (active) {
       double gc[NPH][3], dsum[NPH], mu[NMU], out[NPH];
 #pragma unroll
       for (int a = 0; a < NPH; ++a) {

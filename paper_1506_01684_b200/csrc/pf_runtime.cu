@@ -689,6 +689,7 @@ pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
   kp.pi_eps_4 = M_PI * p->eps / 4.0;
   kp.Gv = p->G * p->v;
   kp.aniso = p->aniso ? 1 : 0;
+  kp.shortcuts = p->shortcuts ? 1 : 0;
   TabParams &tp = c->tp;
   tp.T0 = p->T0; tp.G = p->G; tp.v = p->v; tp.dt = p->dt; tp.dx = p->dx; tp.T_eut = p->T_eut; tp.eps = p->eps;
   for (int a = 0; a < 4; ++a) {

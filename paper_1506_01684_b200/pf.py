@@ -42,7 +42,7 @@ class PfParams(ctypes.Structure):
                 ("L", D * 4), ("D", (D * 2) * 4), ("aniso", I32), ("window", I32), ("window_frac", D),
                 ("window_phi_l", D), ("nan_check_every", I32), ("variant", I32), ("init_kind", I32),
                 ("init_n_seeds", I32), ("init_lam_wmin", I32), ("init_lam_wmax", I32),
-                ("init_planar_phase", I32), ("pad_", I32), ("init_layer_height", D),
+                ("init_planar_phase", I32), ("shortcuts", I32), ("init_layer_height", D),
                 ("init_iface_width", D), ("init_mu_noise", D)]
 
 
@@ -94,7 +94,8 @@ def lib():
 
 def make_params(pd: dict, cfg: dict | None = None, *, layer_height: float | None = None, T0: float | None = None,
                 aniso: bool | None = None, delta_sl: float | None = None, window: bool | None = None,
-                variant: int = 0, nan_check_every: int = 0, nx: int | None = None, ny: int | None = None) -> PfParams:
+                variant: int = 0, nan_check_every: int = 0, nx: int | None = None, ny: int | None = None,
+                shortcuts: bool = False) -> PfParams:
     """PfParams from a params/*.json dict and (optionally) a configs/*.json dict."""
     p = PfParams()
     p.dx, p.dt, p.eps = pd["dx"], pd["dt"], pd["eps"]
@@ -124,6 +125,7 @@ def make_params(pd: dict, cfg: dict | None = None, *, layer_height: float | None
     p.window_phi_l = float((cfg or {}).get("window_front_phi_l", 0.5))
     p.nan_check_every = nan_check_every
     p.variant = variant
+    p.shortcuts = 1 if shortcuts else 0
     kinds = {"voronoi": 0, "lamellar": 1, "planar": 2}
     p.init_kind = kinds[ini.get("kind", "voronoi")]
     if "n_seeds" in ini:

@@ -258,3 +258,35 @@ def test_full_size_sampled_one_step(pv1, name, shape):
     gm = gmu.reshape(2, -1)[:, cells]
     assert O.rel_maxnorm(gp, po) <= TOL1
     assert O.rel_maxnorm(gm, mo) <= TOL1
+
+
+# ---------------------------------------------------------------------------
+# NEXT-1 region shortcuts: bitwise identical to the full update
+# ---------------------------------------------------------------------------
+def _run_variant(pd, cfg, phi, mu, nsteps, shortcuts, blocks=(1, 1, 1), **kw):
+    pf = _pf()
+    nz, ny, nx = phi.shape[1:]
+    prm = pf.make_params(pd, cfg, shortcuts=shortcuts, **kw)
+    with pf.Context(nx, ny, nz, prm, *blocks) as ctx:
+        ctx.write(phi, mu)
+        ctx.step(nsteps)
+        return ctx.read()
+
+
+@pytest.mark.parametrize("name,shape,steps", [("c1", (32, 32, 32), 100), ("c2", (48, 40, 36), 30)])
+def test_shortcuts_bitwise(pv1, name, shape, steps):
+    nx, ny, nz = shape
+    cfg, (phi, mu) = _state(name, nx, ny, nz, layer_height=min(nz // 3, 12))
+    lh = min(nz // 3, 12)
+    a = _run_variant(pv1, cfg, phi, mu, steps, False, layer_height=lh)
+    b = _run_variant(pv1, cfg, phi, mu, steps, True, layer_height=lh)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_shortcuts_bitwise_aniso_window_blocks(pv1):
+    cfg, (phi, mu) = _state("c5", 16, 16, 24, layer_height=16.95, n_seeds=4)
+    pd = dict(pv1, G=0.0)
+    kw = dict(window=True, T0=pv1["T_eut"] - 0.5, layer_height=16.95)
+    a = _run_variant(pd, cfg, phi, mu, 120, False, **kw)
+    b = _run_variant(pd, cfg, phi, mu, 120, True, blocks=(2, 2, 2), **kw)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
