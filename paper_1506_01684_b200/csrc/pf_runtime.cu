@@ -65,6 +65,12 @@ struct pf_ctx {
   int cur = 0;                     // index of the src copy
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // mu-halo overlap: the mu^{n+1} ghost exchange runs on
+  // cstream (with its own communicator) while the next phi-sweep runs on stream
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_mu_done = nullptr, ev_mu_halo = nullptr;
+  bool mu_pending = false;
+  ncclComm_t comm_mu = nullptr;
   double *d_tab = nullptr;
   int64_t tab_planes = 0;
   Plan plan[2][2];                 // [field 0=phi 1=mu][copy]
@@ -375,13 +381,13 @@ size_t ev_next(pf_ctx *c) {
   return c->ev_used++;
 }
 
-struct TimedSpan {  // records an event pair around a group of launches
+struct TimedSpan {  // records an event pair around a group of launches (kind < 0: untimed)
   pf_ctx *c; int kind; size_t e0; int n;
   TimedSpan(pf_ctx *c_, int kind_, int n_) : c(c_), kind(kind_), e0(0), n(n_) {
-    if (c->timing) { e0 = ev_next(c); cudaEventRecord(c->ev[e0], c->stream); }
+    if (c->timing && kind >= 0) { e0 = ev_next(c); cudaEventRecord(c->ev[e0], c->stream); }
   }
   ~TimedSpan() {
-    if (c->timing) {
+    if (c->timing && kind >= 0) {
       const size_t e1 = ev_next(c);
       cudaEventRecord(c->ev[e1], c->stream);
       c->spans.push_back({kind, e0, e1, n});
@@ -389,21 +395,33 @@ struct TimedSpan {  // records an event pair around a group of launches
   }
 };
 
-// Exchange the ghosts of one field in one copy.
-pf_status exchange(pf_ctx *c, int field, int copy) {
+// Exchange the ghosts of one field in one copy, on the
+// main stream, or — `overlap` — on the comm stream with its own communicator
+// (the mu^{n+1} exchange overlapping the next phi-sweep).
+pf_status exchange(pf_ctx *c, int field, int copy, bool overlap = false) {
   const Plan &pl = c->plan[field][copy];
-  TimedSpan ts(c, 2, 0);
-  if (pl.nlocal) { launch_copy(c->stream, pl.d_local, pl.nlocal, pl.max_local); c->launches++; }
+  cudaStream_t st = overlap ? c->cstream : c->stream;
+  ncclComm_t comm = overlap ? c->comm_mu : c->comm;
+  TimedSpan ts(c, overlap ? -1 : 2, 0);
+  if (pl.nlocal) { launch_copy(st, pl.d_local, pl.nlocal, pl.max_local); c->launches++; }
   if (c->g.nranks > 1 && !c->peers[field].empty()) {
     CKN(ncclGroupStart());
     for (const Peer &p : c->peers[field]) {
-      if (p.send_cnt) CKN(ncclSend(c->d_send[field] + p.send_off, (size_t)p.send_cnt, ncclDouble, p.rank, c->comm, c->stream));
-      if (p.recv_cnt) CKN(ncclRecv(c->d_recv[field] + p.recv_off, (size_t)p.recv_cnt, ncclDouble, p.rank, c->comm, c->stream));
+      if (p.send_cnt) CKN(ncclSend(c->d_send[field] + p.send_off, (size_t)p.send_cnt, ncclDouble, p.rank, comm, st));
+      if (p.recv_cnt) CKN(ncclRecv(c->d_recv[field] + p.recv_off, (size_t)p.recv_cnt, ncclDouble, p.rank, comm, st));
     }
     CKN(ncclGroupEnd());
   }
-  if (pl.nunpack) { launch_copy(c->stream, pl.d_unpack, pl.nunpack, pl.max_unpack); c->launches++; }
+  if (pl.nunpack) { launch_copy(st, pl.d_unpack, pl.nunpack, pl.max_unpack); c->launches++; }
   CK(cudaGetLastError());
+  return PF_OK;
+}
+
+// Make the main stream wait for a pending overlapped mu exchange.
+pf_status join_mu(pf_ctx *c) {
+  if (!c->mu_pending) return PF_OK;
+  CK(cudaStreamWaitEvent(c->stream, c->ev_mu_halo, 0));
+  c->mu_pending = false;
   return PF_OK;
 }
 
@@ -744,6 +762,12 @@ pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) { fail(c, PF_ERR_CUDA, "stream"); return bail(PF_ERR_CUDA); }
     c->own_stream = true;
   }
+  if (cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_mu_done, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_mu_halo, cudaEventDisableTiming) != cudaSuccess) {
+    fail(c, PF_ERR_CUDA, "comm stream / events");
+    return bail(PF_ERR_CUDA);
+  }
   c->tab_planes = g->nz + 2;
   if (cudaMalloc(&c->d_tab, (size_t)c->tab_planes * TAB * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&c->d_red, 4 * sizeof(unsigned long long)) != cudaSuccess) {
@@ -754,6 +778,10 @@ pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
     memcpy(&id, g->nccl_id, 128);
     ncclResult_t r = ncclCommInitRank(&c->comm, g->nranks, id, g->rank);
     if (r != ncclSuccess) { fail(c, PF_ERR_COMM, "ncclCommInitRank: %s", ncclGetErrorString(r)); return bail(PF_ERR_COMM); }
+    // a second communicator for the mu exchange, which runs on its own stream
+    // concurrently with the phi-sweep / phi exchange of the next step
+    r = ncclCommSplit(c->comm, 0, g->rank, &c->comm_mu, nullptr);
+    if (r != ncclSuccess) { fail(c, PF_ERR_COMM, "ncclCommSplit: %s", ncclGetErrorString(r)); return bail(PF_ERR_COMM); }
   }
   if (build_plans(c) != PF_OK) return bail(c->status);
   if (cudaDeviceSynchronize() != cudaSuccess) { fail(c, PF_ERR_CUDA, "setup sync"); return bail(PF_ERR_CUDA); }
@@ -870,6 +898,7 @@ pf_status pf_step(pf_ctx *c, int64_t n) {
     }
     CK(cudaGetLastError());
     CKS(exchange(c, 0, c->cur ^ 1));    // lines 2-3: phi_dst ghosts + boundary
+    CKS(join_mu(c));                    // mu_src ghosts (previous step's overlapped exchange)
     {  // mu-sweep (line 4)
       TimedSpan ts(c, 1, (int)c->blocks.size());
       for (const auto &b : c->blocks) {
@@ -880,13 +909,23 @@ pf_status pf_step(pf_ctx *c, int64_t n) {
       }
     }
     CK(cudaGetLastError());
-    CKS(exchange(c, 1, c->cur ^ 1));    // lines 5-6
+    // lines 5-6: mu_dst ghosts + boundary.  The next phi-sweep reads mu at the
+    // cell centre only (D3C1), so this exchange overlaps it
+    // on the comm stream (Algorithm 2's mu communication hiding)
+    CK(cudaEventRecord(c->ev_mu_done, c->stream));
+    CK(cudaStreamWaitEvent(c->cstream, c->ev_mu_done, 0));
+    CKS(exchange(c, 1, c->cur ^ 1, true));
+    CK(cudaEventRecord(c->ev_mu_halo, c->cstream));
+    c->mu_pending = true;
     c->cur ^= 1;                        // line 7: swap
     c->step += 1;
+    const bool nan_due = c->p.nan_check_every > 0 && c->step % c->p.nan_check_every == 0;
+    if ((c->p.window && c->step >= c->next_check) || nan_due) CKS(join_mu(c));
     CKS(window_check(c));
-    if (c->p.nan_check_every > 0 && c->step % c->p.nan_check_every == 0) CKS(nan_check(c));
+    if (nan_due) CKS(nan_check(c));
     if (c->timing && c->spans.size() > 4096) CKS(collect_timing(c));
   }
+  CKS(join_mu(c));
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaGetLastError());
   CKS(collect_timing(c));
@@ -948,7 +987,12 @@ void pf_destroy(pf_ctx *c) {
   if (c->d_red) cudaFree(c->d_red);
   if (c->d_stage) cudaFree(c->d_stage);
   for (auto e : c->ev) cudaEventDestroy(e);
+  if (c->cstream) cudaStreamSynchronize(c->cstream);
+  if (c->comm_mu) ncclCommDestroy(c->comm_mu);
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->ev_mu_done) cudaEventDestroy(c->ev_mu_done);
+  if (c->ev_mu_halo) cudaEventDestroy(c->ev_mu_halo);
+  if (c->cstream) cudaStreamDestroy(c->cstream);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   cudaGetLastError();
   delete c;
