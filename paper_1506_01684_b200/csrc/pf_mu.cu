@@ -57,6 +57,28 @@ struct RawQ {
   __device__ __forceinline__ double dcl(int a, int c) const { return dcl_of(tab, a, c, mu(c)); }
 };
 
+// Accessor for the own column's cell at plane k+1 (the upper cell of the
+// z-face k+1/2): phi^{n+1} and its in-plane gradients from slot sc, phi^n and
+// mu from registers, mobility precomputed; same pinned arithmetic as RawQ /
+// mu_cell_q, so the face has the same bits however its cells were staged.
+struct ColQ {
+  const MuSmem &S;
+  const KParams &kp;
+  int sc, col, row;
+  const double *tab;
+  const double *po, *muv;
+  double Mv[NMU];
+  __device__ __forceinline__ double pn(int a) const { return T(S.pn[sc][a], row, col); }
+  __device__ __forceinline__ double dp(int a) const { return RN_SUB(T(S.pn[sc][a], row, col), po[a]); }
+  __device__ __forceinline__ double gt(int a, int e) const {
+    if (e == 0) return cgrad(kp, T(S.pn[sc][a], row, col - 1), T(S.pn[sc][a], row, col + 1));
+    return cgrad(kp, T(S.pn[sc][a], row - 1, col), T(S.pn[sc][a], row + 1, col));  // e == 1 (z-face: e != 2)
+  }
+  __device__ __forceinline__ double M(int c) const { return Mv[c]; }
+  __device__ __forceinline__ double mu(int c) const { return muv[c]; }
+  __device__ __forceinline__ double dcl(int a, int c) const { return dcl_of(tab, a, c, muv[c]); }
+};
+
 __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid_constant__ TmaMaps tm, KParams kp,
                                                            BlockView b, int kz) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -213,12 +235,14 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
       }
     }
     double fzp[NMU], pn_c[NPH];
-    {  // z-face k+1/2: own cell at k (shared memory) and at k+1 (registers)
+    {  // z-face k+1/2: own cell at k (shared memory) and at k+1 (registers;
+       // the anti-trapping operands are only formed if the guards open)
       RawQ lo = rawq(k, oc, orow);
       lo.Mv[0] = S.M[0][orow][oc]; lo.Mv[1] = S.M[1][orow][oc];
-      MuQ qn;
-      own_q(k + 1, po_n, mu_n, qn);
-      mu_face_t(kp, lo, MuQAcc{qn}, 2, fzp);
+      const int s1 = slot(k + 1);
+      ColQ hi{S, kp, s1, oc, orow, S.tab[s1], po_n, mu_n,
+              {mob_of(S.tab[s1], 0, po_n), mob_of(S.tab[s1], 1, po_n)}};
+      mu_face_t(kp, lo, hi, 2, fzp);
 #pragma unroll
       for (int a = 0; a < NPH; ++a) pn_c[a] = T(S.pn[sn][a], orow, oc);
     }
