@@ -20,14 +20,13 @@ namespace pf {
 
 struct __align__(128) PhiSmem {
   double p[NSLOT][NPH][TSZ];       // phi^n tile planes, (row, col) at row * RX + col
-  double mu[NSLOT][NMU][TY * TX];  // mu^n of the interior cells
   double tab[NSLOT][TAB];          // per-plane table rows
-  double fx[1][NPH][TY][TX + 1];   // x-face fluxes at i - 1/2, i = 0..TX
-  double fy[1][NPH][TY + 1][TX];   // y-face fluxes at j - 1/2, j = 0..TY
+  double fx[2][NPH][TY][TX + 1];   // x-face fluxes at i - 1/2, i = 0..TX (plane parity)
+  double fy[2][NPH][TY + 1][TX];   // y-face fluxes at j - 1/2, j = 0..TY
   uint64_t bar[NSLOT];             // one mbarrier per slot
 };
 
-constexpr uint32_t PHI_STAGE_BYTES = (NPH * RXS * RY + NMU * TX * TY + TAB) * 8;
+constexpr uint32_t PHI_STAGE_BYTES = (NPH * RXS * RY + TAB) * 8;
 
 template <bool ANISO>
 __global__ void __launch_bounds__(NTHR, 512 / NTHR) phi_tiled_kernel(const __grid_constant__ TmaMaps tm, KParams kp, BlockView b,
@@ -53,8 +52,6 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) phi_tiled_kernel(const __gri
     const int z = k + b.zoff;
 #pragma unroll
     for (int a = 0; a < NPH; ++a) tma_load_3d(S.p[s][a], &tm.phi[a], i0 - 2 + XO, j0, z, &S.bar[s]);
-#pragma unroll
-    for (int c = 0; c < NMU; ++c) tma_load_3d(S.mu[s][c], &tm.mui[c], i0 + XO, j0 + 1, z, &S.bar[s]);
     bulk_load(S.tab[s], b.tab + (int64_t)k * TAB, TAB * 8, &S.bar[s]);
   };
   auto wait = [&](int k) { mbar_wait(&S.bar[slot(k)], parity(k)); };
@@ -100,17 +97,28 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) phi_tiled_kernel(const __gri
     phi_face(kp, lo, hi, ANISO ? gl : gdum, ANISO ? gh : gdum, 2, jzm);
   }
 
-  // Two CTA barriers per plane: C (faces of plane k-1 consumed) and B (faces of
-  // plane k complete).  A single barrier with plane-parity face buffers was
-  // measured slower: the second buffer costs a CTA per SM of occupancy.
-  // TMA refills slot(k+2) = slot(k-2), last read in D(k-1), before B(k-1).
+  // One CTA barrier per plane (B): the face buffers alternate by plane parity,
+  // so D(k) never overwrites faces another thread may still read in F(k-1);
+  // buffer (k & 1) was last read in F(k-2), which every thread finished before
+  // reaching B(k-1).  TMA refills slot(k+2) = slot(k-2), last read in D(k-1),
+  // likewise before B(k-1).  mu (D3C1: the cell's own value) comes straight
+  // from global memory one plane ahead, which keeps the shared footprint at
+  // 4 CTAs / SM.
+  double mu_n[NMU];
+#pragma unroll
+  for (int c = 0; c < NMU; ++c) mu_n[c] = active ? __ldg(b.mu[c] + (int64_t)k0 * b.plane + colo) : 0.0;
   for (int k = k0; k < k1; ++k) {
     // A: stage plane k+2 (needed from iteration k+1 on); wait for plane k+1
     if (tid == 0 && k + 2 <= k1) stage(k + 2);
+    double mu_c[NMU];
+#pragma unroll
+    for (int c = 0; c < NMU; ++c) {
+      mu_c[c] = mu_n[c];
+      mu_n[c] = (active && k + 1 < k1) ? __ldg(b.mu[c] + (int64_t)(k + 1) * b.plane + colo) : 0.0;
+    }
     wait(k + 1);
-    __syncthreads();  // C
     const int sc = slot(k), sm = slot(k - 1), sp = slot(k + 1);
-    const int fb = 0;
+    const int fb = (k - k0) & 1;
     // D: faces of plane k; own column values to registers
     double pm[NPH], pc[NPH], pp[NPH], jzp[NPH];
     {
@@ -198,8 +206,8 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) phi_tiled_kernel(const __gri
         dsum[a] = ((S.fx[fb][a][ty][tx + 1] - S.fx[fb][a][ty][tx]) + (S.fy[fb][a][ty + 1][tx] - S.fy[fb][a][ty][tx])) +
                   (jzp[a] - jzm[a]);
       }
-      mu[0] = S.mu[sc][0][ty * TX + tx];
-      mu[1] = S.mu[sc][1][ty * TX + tx];
+      mu[0] = mu_c[0];
+      mu[1] = mu_c[1];
       phi_cell_update_div(kp, S.tab[sc], pc, mu, gc, dsum, out);
       const int64_t o = (int64_t)k * b.plane + colo;
 #pragma unroll
