@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
   const int bx = i0 - 2 + XO, by = j0;  // tile box origin (16-byte aligned x)
   auto stage_pn = [&](int k) {            // phi^{n+1} tiles + table row of plane k
     const int s = slot(k);
-    fence_proxy_async();
+    // no proxy fence (WAR ordered by the CTA barrier; see pf_phi.cu)
     mbar_expect_tx(&S.bar_pn[s], MU_PN_BYTES);
 #pragma unroll
     for (int a = 0; a < NPH; ++a) tma_load_3d(S.pn[s][a], &tm.phin[a], bx, by, k + b.zoff, &S.bar_pn[s]);
@@ -111,7 +111,6 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
   };
   auto stage_pm = [&](int k) {            // phi^n and mu tiles of plane k
     const int s = slot2(k);
-    fence_proxy_async();
     mbar_expect_tx(&S.bar_pm[s], MU_PM_BYTES);
 #pragma unroll
     for (int a = 0; a < NPH; ++a) tma_load_3d(S.po[s][a], &tm.phi[a], bx, by, k + b.zoff, &S.bar_pm[s]);

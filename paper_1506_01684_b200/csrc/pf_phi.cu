@@ -47,7 +47,9 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) phi_tiled_kernel(const __gri
   // plane k -> its slot: 4 phi tiles, 2 mu interior boxes, the table row
   auto stage = [&](int k) {
     const int s = slot(k);
-    fence_proxy_async();
+    // no proxy fence: the slot's last (generic) reads are ordered before this
+    // (async) refill by the CTA barrier; a fence here costs a MEMBAR that waits
+    // for the issuing warp's outstanding global stores
     mbar_expect_tx(&S.bar[s], PHI_STAGE_BYTES);
     const int z = k + b.zoff;
 #pragma unroll
