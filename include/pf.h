@@ -23,7 +23,8 @@
  *    n = nx_l*ny_l*nz_l.  Pointers may be host or device memory (detected).
  *  - Boundaries: periodic in x and y, zero-flux (zero-gradient ghosts) in z.
  *  - Every function returns pf_status; no C++ exception crosses the ABI.  After
- *    any error the context is poisoned: later calls return PF_ERR_STATE, and
+ *    any error except PF_ERR_IO the context is poisoned: later calls return
+ *    PF_ERR_STATE, and
  *    pf_last_error() describes the first failure.  A context is
  *    single-thread-affine.
  *  - Ownership: the context owns every device allocation (fields, halo
@@ -47,7 +48,10 @@ typedef enum {
   PF_ERR_CUDA = -3,      /* a CUDA runtime error (message in pf_last_error)        */
   PF_ERR_COMM = -4,      /* an NCCL error                                          */
   PF_ERR_STATE = -5,     /* call out of order (step before init) or after an error */
-  PF_ERR_ARG = -6        /* NULL or out-of-range argument                          */
+  PF_ERR_ARG = -6,       /* NULL or out-of-range argument                          */
+  PF_ERR_IO = -7         /* checkpoint file error (open/read/write, bad magic,
+                            header not matching the grid, truncated body); does
+                            NOT poison the context (see pf_save / pf_load)       */
 } pf_status;
 
 /* Grid and decomposition (copied by pf_create).  The global nx*ny*nz interior
@@ -157,6 +161,34 @@ pf_status pf_step(pf_ctx *c, int64_t n);
 
 /* Copy the rank's interior state out (layout above; host or device). */
 pf_status pf_read(pf_ctx *c, double *phi, double *mu);
+
+/* FP32 checkpoint of the current state (§Input/Output: "the
+ * complete simulation state ... four phi values and two mu values per cell ...
+ * checkpoints use only single precision").  Collective over the context's
+ * ranks; every rank writes its own rows of the one shared file `path`
+ * (created / truncated by rank 0).  Format, little endian:
+ *     bytes  0..7   magic "PFCP0001"
+ *            8..31  u64 NX, NY, NZ (global interior)
+ *           32..39  u32 N = 4 phases, u32 K-1 = 2 potentials
+ *           40..55  f64 dx, f64 t = step * dt
+ *           56..71  u64 step, u64 window origin (global plane of k = 0)
+ *     body          binary32, component-major: phi_0..phi_3 then mu_0, mu_1,
+ *                   each NX*NY*NZ values x fastest, (k*NY + j)*NX + i
+ * Values are the IEEE round-to-nearest-even binary32 casts of the binary64
+ * state.  Errors: PF_ERR_STATE before pf_init/pf_write/pf_load, PF_ERR_ARG,
+ * PF_ERR_IO (context still usable; a partial file may remain), PF_ERR_CUDA /
+ * PF_ERR_COMM. */
+pf_status pf_save(pf_ctx *c, const char *path);
+
+/* Restore a checkpoint written by pf_save (any decomposition): the state
+ * becomes the binary64 widening of the stored binary32 values (exact), step
+ * and window origin come from the header (t is not read back: t = step * dt);
+ * all ghosts are filled.  Collective.  The header must match the context
+ * (NX, NY, NZ, N, K-1, dx bit for bit) and the body be complete, else
+ * PF_ERR_IO with the state untouched; a read failure after the header checks
+ * returns PF_ERR_IO and leaves the context uninitialized (pf_step returns
+ * PF_ERR_STATE until the next pf_init / pf_write / pf_load). */
+pf_status pf_load(pf_ctx *c, const char *path);
 
 /* Enable (1) / disable (0) per-sweep CUDA-event timing; resets the timers. */
 pf_status pf_set_timing(pf_ctx *c, int32_t on);

@@ -360,4 +360,25 @@ void launch_gather(cudaStream_t s, const double *const f[NPH], int ncomp, int nx
                                         plane, dst, dnx, dny, dn, ox, oy, oz, scatter ? 1 : 0);
 }
 
+// FP32 checkpoint conversion: one padded binary64 component
+// <-> a compact binary32 box (x fastest) at offset (ox, oy, oz) inside a
+// dnx*dny*... array.  double -> float is the IEEE round-to-nearest-even cast,
+// float -> double is exact.
+__global__ void cvt32_kernel(double *f, int nx, int ny, int nz, int64_t pitch, int64_t plane, float *dst,
+                             int64_t dnx, int64_t dny, int64_t ox, int64_t oy, int64_t oz, int to_fields) {
+  const int64_t n = (int64_t)nx * ny * nz;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % nx, j = (t / nx) % ny, k = t / ((int64_t)nx * ny);
+    const int64_t o = k * plane + j * pitch + i;
+    const int64_t d = ((oz + k) * dny + (oy + j)) * dnx + (ox + i);
+    if (to_fields) f[o] = (double)dst[d];
+    else dst[d] = __double2float_rn(f[o]);
+  }
+}
+
+void launch_cvt32(cudaStream_t s, double *f, int nx, int ny, int nz, int64_t pitch, int64_t plane, float *dst,
+                  int64_t dnx, int64_t dny, int64_t ox, int64_t oy, int64_t oz, bool to_fields) {
+  cvt32_kernel<<<148 * 8, 256, 0, s>>>(f, nx, ny, nz, pitch, plane, dst, dnx, dny, ox, oy, oz, to_fields ? 1 : 0);
+}
+
 }  // namespace pf

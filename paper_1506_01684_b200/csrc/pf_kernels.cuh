@@ -80,5 +80,7 @@ void launch_nancheck(cudaStream_t s, const double *const f[NPH], int ncomp, int 
 void launch_gather(cudaStream_t s, const double *const f[NPH], int ncomp, int nx, int ny, int nz, int64_t pitch,
                    int64_t plane, double *dst, int64_t dnx, int64_t dny, int64_t dn, int64_t ox, int64_t oy, int64_t oz,
                    bool scatter, double *const fw[NPH]);
+void launch_cvt32(cudaStream_t s, double *f, int nx, int ny, int nz, int64_t pitch, int64_t plane, float *dst,
+                  int64_t dnx, int64_t dny, int64_t ox, int64_t oy, int64_t oz, bool to_fields);
 
 }  // namespace pf

@@ -7,8 +7,12 @@
 // send/recv), the moving window and the
 // NaN watchdog ("no silent NaN propagation").
 #include <cuda_runtime.h>
+#include <fcntl.h>
 #include <nccl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
+#include <cerrno>
 #include <algorithm>
 #include <array>
 #include <cmath>
@@ -595,6 +599,112 @@ pf_status move_state(pf_ctx *c, double *phi, double *mu, bool to_fields) {
   return PF_OK;
 }
 
+// ---------------------------------------------------------------------------
+// FP32 checkpoints: "four phi values and two mu values per
+// cell ... checkpoints use only single precision".  File = 72-byte header
+// (magic "PFCP0001", u64 NX NY NZ, u32 N, u32 K-1, f64 dx, f64 t, u64 step,
+// u64 window origin; little endian) + component-major binary32 body (all
+// phi_0, ..., phi_3, mu_0, mu_1; each x fastest over the global grid;
+// SPEC.md:462-466).  Every rank converts its blocks on the device in z-chunks
+// and writes / reads its own rows with pwrite / pread, the host I/O of chunk
+// i overlapping the conversion + PCIe copy of chunk i+1.
+// ---------------------------------------------------------------------------
+static_assert(__BYTE_ORDER__ == __ORDER_LITTLE_ENDIAN__, "checkpoint format is little endian");
+constexpr int64_t CKPT_HDR = 72;
+constexpr int64_t CKPT_CHUNK = 8 << 20;  // floats per conversion chunk (32 MB)
+
+// I/O and format errors do not poison the context (message in pf_last_error)
+pf_status io_fail(pf_ctx *c, const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c->status == PF_OK) c->err = buf;
+  return PF_ERR_IO;
+}
+
+// collective "did any rank fail?" (an allreduce(max) of the local error flag);
+// also orders the ranks' file accesses
+pf_status io_agree(pf_ctx *c, pf_status local) {
+  if (c->g.nranks == 1) return local;
+  const unsigned long long flag = local != PF_OK;
+  CK(cudaMemcpyAsync(c->d_red + 3, &flag, sizeof(flag), cudaMemcpyHostToDevice, c->stream));
+  CKN(ncclAllReduce(c->d_red + 3, c->d_red + 3, 1, ncclUint64, ncclMax, c->comm, c->stream));
+  unsigned long long any = 0;
+  CK(cudaMemcpyAsync(&any, c->d_red + 3, sizeof(any), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (local != PF_OK) return local;
+  return any ? io_fail(c, "checkpoint I/O failed on another rank") : PF_OK;
+}
+
+struct CkptChunk { int blk, q; int kz0, nzc; };
+
+std::vector<CkptChunk> ckpt_chunks(const pf_ctx *c) {
+  std::vector<CkptChunk> v;
+  for (int q = 0; q < NPH + NMU; ++q)
+    for (int bi = 0; bi < (int)c->blocks.size(); ++bi) {
+      const Block &b = c->blocks[bi];
+      const int nzc = (int)std::max<int64_t>(1, CKPT_CHUNK / ((int64_t)b.nx * b.ny));
+      for (int k = 0; k < b.nz; k += nzc) v.push_back({bi, q, k, std::min(nzc, b.nz - k)});
+    }
+  return v;
+}
+
+// pwrite / pread the rows of one chunk (host buffer compact, x fastest),
+// merging rows that are contiguous in the file
+bool ckpt_rows(const pf_ctx *c, int fd, const CkptChunk &ch, float *h, bool write) {
+  const Block &b = c->blocks[ch.blk];
+  const int64_t NX = c->g.nx, NY = c->g.ny, NXYZ = NX * NY * c->g.nz;
+  const int64_t rows = (int64_t)ch.nzc * b.ny, rowb = (int64_t)b.nx * 4;
+  int64_t r = 0;
+  while (r < rows) {
+    auto off = [&](int64_t row) {
+      const int64_t k = row / b.ny, j = row % b.ny;
+      return CKPT_HDR + 4 * ((int64_t)ch.q * NXYZ + ((b.z0 + ch.kz0 + k) * NY + (b.y0 + j)) * NX + b.x0);
+    };
+    int64_t r1 = r + 1;
+    while (r1 < rows && off(r1) == off(r) + (r1 - r) * rowb) ++r1;
+    char *p = reinterpret_cast<char *>(h + r * b.nx);
+    int64_t len = (r1 - r) * rowb, o = off(r);
+    while (len > 0) {
+      const ssize_t d = write ? pwrite(fd, p, (size_t)len, o) : pread(fd, p, (size_t)len, o);
+      if (d <= 0) return false;
+      p += d; o += d; len -= d;
+    }
+    r = r1;
+  }
+  return true;
+}
+
+struct CkptBuffers {  // two pinned host chunk buffers + one device chunk buffer
+  float *h[2] = {nullptr, nullptr}, *d = nullptr;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  ~CkptBuffers() {
+    for (int s = 0; s < 2; ++s) { if (h[s]) cudaFreeHost(h[s]); if (ev[s]) cudaEventDestroy(ev[s]); }
+    if (d) cudaFree(d);
+  }
+};
+
+pf_status ckpt_alloc(pf_ctx *c, CkptBuffers &cb) {
+  int64_t m = 1;
+  for (const auto &b : c->blocks)
+    m = std::max(m, std::min<int64_t>((int64_t)b.nx * b.ny * b.nz,
+                                      std::max<int64_t>(CKPT_CHUNK / ((int64_t)b.nx * b.ny), 1) * b.nx * b.ny));
+  for (int s = 0; s < 2; ++s) {
+    CK(cudaMallocHost(&cb.h[s], (size_t)m * 4));
+    CK(cudaEventCreateWithFlags(&cb.ev[s], cudaEventDisableTiming));
+  }
+  CK(cudaMalloc(&cb.d, (size_t)m * 4));
+  return PF_OK;
+}
+
+void ckpt_convert(pf_ctx *c, const CkptChunk &ch, float *d, bool to_fields) {
+  const Block &b = c->blocks[ch.blk];
+  double *f = field_ptr(b, ch.q < NPH ? 0 : 1, c->cur, ch.q < NPH ? ch.q : ch.q - NPH) + cell_off(b, 0, 0, ch.kz0);
+  launch_cvt32(c->stream, f, b.nx, b.ny, ch.nzc, b.pitch, b.plane, d, b.nx, b.ny, 0, 0, 0, to_fields);
+}
+
 pf_status validate(const pf_grid *g, const pf_params *p) {
   pf_ctx *c = nullptr;
   const int64_t n[3] = {g->nx, g->ny, g->nz};
@@ -936,6 +1046,129 @@ pf_status pf_read(pf_ctx *c, double *phi, double *mu) {
   CKS(check_state(c, true));
   if (!phi || !mu) return fail(c, PF_ERR_ARG, "NULL state pointer");
   return move_state(c, phi, mu, false);
+}
+
+pf_status pf_save(pf_ctx *c, const char *path) {
+  CKS(check_state(c, true));
+  if (!path) return fail(c, PF_ERR_ARG, "NULL path");
+  CKS(join_mu(c));
+  pf_status st = PF_OK;
+  if (c->g.rank == 0) {  // header + full-length file, before any rank writes rows
+    unsigned char hdr[CKPT_HDR];
+    const uint64_t dims[3] = {(uint64_t)c->g.nx, (uint64_t)c->g.ny, (uint64_t)c->g.nz};
+    const uint32_t counts[2] = {NPH, NMU};
+    const double dx = c->p.dx, t = (double)c->step * c->p.dt;
+    const uint64_t tail[2] = {(uint64_t)c->step, (uint64_t)c->zorig};
+    memcpy(hdr, "PFCP0001", 8);
+    memcpy(hdr + 8, dims, 24);
+    memcpy(hdr + 32, counts, 8);
+    memcpy(hdr + 40, &dx, 8);
+    memcpy(hdr + 48, &t, 8);
+    memcpy(hdr + 56, tail, 16);
+    const int64_t total = CKPT_HDR + (int64_t)(NPH + NMU) * c->g.nx * c->g.ny * c->g.nz * 4;
+    const int fd = open(path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
+    if (fd < 0) st = io_fail(c, "pf_save: cannot create %s: %s", path, strerror(errno));
+    else {
+      if (pwrite(fd, hdr, CKPT_HDR, 0) != CKPT_HDR || ftruncate(fd, total) != 0)
+        st = io_fail(c, "pf_save: writing %s: %s", path, strerror(errno));
+      close(fd);
+    }
+  }
+  CKS(io_agree(c, st));
+  CkptBuffers cb;
+  CKS(ckpt_alloc(c, cb));
+  const int fd = open(path, O_WRONLY);
+  if (fd < 0) st = io_fail(c, "pf_save: cannot open %s: %s", path, strerror(errno));
+  const auto chunks = ckpt_chunks(c);
+  for (size_t i = 0; i <= chunks.size() && st == PF_OK; ++i) {
+    if (i < chunks.size()) {  // device: FP64 -> FP32 + copy out of chunk i into slot i % 2
+      const CkptChunk &ch = chunks[i];
+      const Block &b = c->blocks[ch.blk];
+      ckpt_convert(c, ch, cb.d, false);
+      CK(cudaMemcpyAsync(cb.h[i & 1], cb.d, (size_t)b.nx * b.ny * ch.nzc * 4, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaEventRecord(cb.ev[i & 1], c->stream));
+    }
+    if (i > 0) {  // host: write chunk i - 1 while the device works on chunk i
+      CK(cudaEventSynchronize(cb.ev[(i - 1) & 1]));
+      if (!ckpt_rows(c, fd, chunks[i - 1], cb.h[(i - 1) & 1], true))
+        st = io_fail(c, "pf_save: writing %s: %s", path, strerror(errno));
+    }
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  if (fd >= 0 && close(fd) != 0 && st == PF_OK) st = io_fail(c, "pf_save: closing %s: %s", path, strerror(errno));
+  return io_agree(c, st);
+}
+
+pf_status pf_load(pf_ctx *c, const char *path) {
+  CKS(check_state(c, false));
+  if (!path) return fail(c, PF_ERR_ARG, "NULL path");
+  CKS(join_mu(c));
+  pf_status st = PF_OK;
+  uint64_t step = 0, zorig = 0;
+  const int fd = open(path, O_RDONLY);
+  if (fd < 0) st = io_fail(c, "pf_load: cannot open %s: %s", path, strerror(errno));
+  else {
+    unsigned char hdr[CKPT_HDR];
+    uint64_t dims[3];
+    uint32_t counts[2];
+    double dx;
+    struct stat sb;
+    const int64_t total = CKPT_HDR + (int64_t)(NPH + NMU) * c->g.nx * c->g.ny * c->g.nz * 4;
+    if (pread(fd, hdr, CKPT_HDR, 0) != CKPT_HDR || fstat(fd, &sb) != 0)
+      st = io_fail(c, "pf_load: %s: truncated header", path);
+    else if (memcmp(hdr, "PFCP0001", 8) != 0)
+      st = io_fail(c, "pf_load: %s: bad magic (not a PFCP0001 checkpoint)", path);
+    else {
+      memcpy(dims, hdr + 8, 24);
+      memcpy(counts, hdr + 32, 8);
+      memcpy(&dx, hdr + 40, 8);
+      memcpy(&step, hdr + 56, 8);
+      memcpy(&zorig, hdr + 64, 8);
+      if (dims[0] != (uint64_t)c->g.nx || dims[1] != (uint64_t)c->g.ny || dims[2] != (uint64_t)c->g.nz)
+        st = io_fail(c, "pf_load: %s: grid %llux%llux%llu does not match the context's %lldx%lldx%lld", path,
+                     (unsigned long long)dims[0], (unsigned long long)dims[1], (unsigned long long)dims[2],
+                     (long long)c->g.nx, (long long)c->g.ny, (long long)c->g.nz);
+      else if (counts[0] != NPH || counts[1] != NMU)
+        st = io_fail(c, "pf_load: %s: %u phases / %u potentials, expected %d / %d", path, counts[0], counts[1], NPH, NMU);
+      else if (dx != c->p.dx)
+        st = io_fail(c, "pf_load: %s: dx %.17g differs from the context's %.17g", path, dx, c->p.dx);
+      else if ((int64_t)sb.st_size < total)
+        st = io_fail(c, "pf_load: %s: truncated body (%lld of %lld bytes)", path, (long long)sb.st_size,
+                     (long long)total);
+    }
+  }
+  st = io_agree(c, st);
+  if (st != PF_OK) { if (fd >= 0) close(fd); return st; }
+  // the fields are overwritten from here on: a failure leaves no valid state
+  c->initialized = false;
+  for (auto &b : c->blocks) b.woff = 0;
+  c->cur = 0;
+  CKS(build_plans(c));
+  CkptBuffers cb;
+  CKS(ckpt_alloc(c, cb));
+  const auto chunks = ckpt_chunks(c);
+  for (size_t i = 0; i < chunks.size() && st == PF_OK; ++i) {
+    const CkptChunk &ch = chunks[i];
+    const Block &b = c->blocks[ch.blk];
+    if (i >= 2) CK(cudaEventSynchronize(cb.ev[i & 1]));  // slot free: its copy-in finished
+    // host: read chunk i while the device converts chunk i - 1
+    if (!ckpt_rows(c, fd, ch, cb.h[i & 1], false)) { st = io_fail(c, "pf_load: reading %s failed", path); break; }
+    CK(cudaMemcpyAsync(cb.d, cb.h[i & 1], (size_t)b.nx * b.ny * ch.nzc * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaEventRecord(cb.ev[i & 1], c->stream));
+    ckpt_convert(c, ch, cb.d, true);
+  }
+  close(fd);
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaGetLastError());
+  CKS(io_agree(c, st));
+  CKS(fill_all_ghosts(c));
+  CK(cudaStreamSynchronize(c->stream));
+  c->step = (int64_t)step;
+  c->zorig = (int64_t)zorig;
+  c->next_check = c->step;
+  c->last_front = -1;
+  c->initialized = true;
+  return PF_OK;
 }
 
 pf_status pf_set_timing(pf_ctx *c, int32_t on) {

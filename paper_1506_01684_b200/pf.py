@@ -22,11 +22,12 @@ D = ctypes.c_double
 I32 = ctypes.c_int32
 I64 = ctypes.c_int64
 
-PF_OK, PF_ERR_CONFIG, PF_ERR_NUMERICAL, PF_ERR_CUDA, PF_ERR_COMM, PF_ERR_STATE, PF_ERR_ARG = 0, -1, -2, -3, -4, -5, -6
+PF_OK, PF_ERR_CONFIG, PF_ERR_NUMERICAL, PF_ERR_CUDA, PF_ERR_COMM, PF_ERR_STATE, PF_ERR_ARG, PF_ERR_IO = \
+    0, -1, -2, -3, -4, -5, -6, -7
 STATUS_NAMES = {0: "PF_OK", -1: "PF_ERR_CONFIG", -2: "PF_ERR_NUMERICAL", -3: "PF_ERR_CUDA", -4: "PF_ERR_COMM",
-                -5: "PF_ERR_STATE", -6: "PF_ERR_ARG"}
+                -5: "PF_ERR_STATE", -6: "PF_ERR_ARG", -7: "PF_ERR_IO"}
 EXPORTS = ["pf_nccl_unique_id", "pf_halo_plan", "pf_create", "pf_init", "pf_write", "pf_set_time", "pf_step", "pf_read",
-           "pf_set_timing", "pf_info", "pf_last_error", "pf_destroy"]
+           "pf_save", "pf_load", "pf_set_timing", "pf_info", "pf_last_error", "pf_destroy"]
 
 
 class PfGrid(ctypes.Structure):
@@ -79,6 +80,8 @@ def lib():
         L.pf_set_time.argtypes = [vp, I64, I64]
         L.pf_step.argtypes = [vp, I64]
         L.pf_read.argtypes = [vp, vp, vp]
+        L.pf_save.argtypes = [vp, ctypes.c_char_p]
+        L.pf_load.argtypes = [vp, ctypes.c_char_p]
         L.pf_set_timing.argtypes = [vp, I32]
         L.pf_info.argtypes = [vp, ctypes.POINTER(PfInfo)]
         L.pf_last_error.argtypes = [vp]
@@ -212,6 +215,14 @@ class Context:
             mu = np.empty((2,) + self.shape)
         self._check(lib().pf_read(self._c, _ptr(phi), _ptr(mu)))
         return phi, mu
+
+    def save(self, path):
+        """FP32 checkpoint of the current state (pf_save; collective)."""
+        self._check(lib().pf_save(self._c, os.fsencode(path)))
+
+    def load(self, path):
+        """Restore a pf_save checkpoint (pf_load; collective)."""
+        self._check(lib().pf_load(self._c, os.fsencode(path)))
 
     def set_timing(self, on: bool):
         self._check(lib().pf_set_timing(self._c, 1 if on else 0))

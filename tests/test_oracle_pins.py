@@ -486,3 +486,60 @@ def test_p14_roofline_arithmetic():
     assert round(80 * 2 ** 30 / 680 / 1e6, 1) == 126.3
     assert round(4.2e6 * 1384 / 1e9, 1) == 5.8
     assert round(5.8 / 21.6 * 100) == 27
+
+
+# ---------------------------------------------------------------------------
+# P15: FP32 checkpoint format (NEXT-3)
+# ---------------------------------------------------------------------------
+def _golden_bytes(name):
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", name)
+    hexs = " ".join(line.split("#", 1)[0] for line in open(path))
+    return bytes.fromhex("".join(hexs.split()))
+
+
+def test_p15_checkpoint_matches_hand_assembled_bytes():
+    from oracle import checkpoint as CK
+    phi = np.array([[1.0, 0.1], [0.0, 1 / 3], [0.0, 0.5], [0.0, 0.0625]]).reshape(4, 1, 1, 2)
+    mu = np.array([[1 + 2.0 ** -24, 1 + 3 * 2.0 ** -24], [-2.0, 1e-50]]).reshape(2, 1, 1, 2)
+    want = _golden_bytes("checkpoint_2x1x1.hex")
+    assert len(want) == 72 + 6 * 2 * 4
+    assert CK.encode(phi, mu, dx=1.0, t=0.3, step=10, z_origin=7) == want
+    hdr, p32, m32 = CK.decode(want)
+    assert hdr == dict(nx=2, ny=1, nz=1, n_phases=4, n_mu=2, dx=1.0, t=0.3, step=10, z_origin=7)
+    # round-to-nearest-even ties and underflow, read back as exact binary32 values
+    assert m32[0, 0, 0, 0] == 1.0 and m32[0, 0, 0, 1] == 1 + 2.0 ** -22 and m32[1, 0, 0, 1] == 0.0
+
+
+def test_p15_checkpoint_roundtrip_is_binary32_cast_and_size(tmp_path):
+    from oracle import checkpoint as CK
+    rng = np.random.default_rng(5)
+    phi = rng.standard_normal((4, 5, 3, 7)) * 10.0 ** rng.integers(-44, 36, (4, 5, 3, 7))
+    mu = rng.standard_normal((2, 5, 3, 7))
+    p = tmp_path / "c.pfcp"
+    CK.write_checkpoint(p, phi, mu, dx=0.5, t=1.25, step=3, z_origin=11)
+    assert p.stat().st_size == 72 + 6 * 5 * 3 * 7 * 4
+    hdr, p32, m32 = CK.decode(p.read_bytes())
+    assert (hdr["nx"], hdr["ny"], hdr["nz"], hdr["step"], hdr["z_origin"]) == (7, 3, 5, 3, 11)
+    # each stored value is the float32 nearest to the original (ties: even); check
+    # by brute force against its two float32 neighbours
+    for orig, got in ((phi, p32), (mu, m32)):
+        g = got.astype(np.float64)
+        up = np.nextafter(got, np.float32(np.inf)).astype(np.float64)
+        dn = np.nextafter(got, np.float32(-np.inf)).astype(np.float64)
+        fin = np.isfinite(g) & (np.abs(orig) < 3e38)
+        assert np.all(np.abs(orig - g)[fin] <= np.abs(orig - up)[fin])
+        assert np.all(np.abs(orig - g)[fin] <= np.abs(orig - dn)[fin])
+    # size of a 64^3 checkpoint
+    assert len(CK.encode(np.zeros((4, 64, 64, 64)), np.zeros((2, 64, 64, 64)), 1.0, 0.0, 0, 0)) == 72 + 6 * 64 ** 3 * 4
+
+
+def test_p15_checkpoint_rejects_bad_files():
+    from oracle import checkpoint as CK
+    good = _golden_bytes("checkpoint_2x1x1.hex")
+    with pytest.raises(CK.CheckpointError):
+        CK.decode(b"XFCP0001" + good[8:])
+    with pytest.raises(CK.CheckpointError):
+        CK.decode(good[:-1])
+    with pytest.raises(CK.CheckpointError):
+        CK.decode(good[:40])
