@@ -543,3 +543,143 @@ def test_p15_checkpoint_rejects_bad_files():
         CK.decode(good[:-1])
     with pytest.raises(CK.CheckpointError):
         CK.decode(good[:40])
+
+
+# ---------------------------------------------------------------------------
+# P16: marching cubes (NEXT-4, reading R26)
+# ---------------------------------------------------------------------------
+def _tri_normals(pos):
+    return np.cross(pos[:, 1] - pos[:, 0], pos[:, 2] - pos[:, 0])
+
+
+def _unwrap(pos, Lx, Ly):
+    """Minimal-image copy of each triangle (vertex x, y are wrapped into the
+    periodic box, so a triangle on the seam has vertices on both sides)."""
+    pos = pos.copy()
+    for ax, L in ((0, Lx), (1, Ly)):
+        d = pos[:, 1:, ax] - pos[:, :1, ax]
+        pos[:, 1:, ax] -= np.round(d / L) * L
+    return pos
+
+
+def _unpaired_directed_edges(ids, skip=lambda a, b: False):
+    from collections import Counter
+    E = Counter()
+    for tr in ids:
+        for s in range(3):
+            E[(int(tr[s]), int(tr[(s + 1) % 3]))] += 1
+    return [e for e in E if not skip(*e) and (E[e] != 1 or E.get((e[1], e[0]), 0) != 1)]
+
+
+def test_p16_uniform_field_gives_empty_mesh():
+    from oracle import mesh as MC
+    for v in (0.0, 0.3, 0.5, 0.9, 1.0):
+        ids, pos = MC.marching_cubes(np.full((5, 4, 6), v))
+        assert ids.shape == (0, 3) and pos.shape == (0, 3, 3)
+
+
+def test_p16_plane_area_and_orientation():
+    from oracle import mesh as MC
+    NX, NY, NZ, dx = 7, 5, 6, 0.5
+    z = np.arange(NZ) + 0.5
+    phi = np.broadcast_to((0.5 + 0.2 * (2.8 - z))[:, None, None], (NZ, NY, NX))   # solid below z = 2.8
+    ids, pos = MC.marching_cubes(phi, dx=dx)
+    assert pos[:, :, :2].min() >= 0.5 * dx and pos[:, :, :2].max() <= (max(NX, NY) - 0.5) * dx
+    n = _tri_normals(_unwrap(pos, NX * dx, NY * dx))
+    assert np.allclose(pos[:, :, 2], 2.8 * dx, rtol=0, atol=1e-14)
+    assert abs(0.5 * np.linalg.norm(n, axis=1).sum() - NX * NY * dx * dx) < 1e-12
+    assert np.all(n[:, 2] > 0) and np.allclose(n[:, :2], 0)      # out of the phase: +z
+
+
+def test_p16_sphere_area_volume_euler():
+    # SPEC.md:489: radius 10 dx sphere -> closed, chi = 2, area / volume within 2 %
+    from oracle import mesh as MC
+    N, R = 32, 10.0
+    z, y, x = np.meshgrid(*(np.arange(N) + 0.5,) * 3, indexing="ij")
+    r = np.sqrt((x - 16.2) ** 2 + (y - 15.9) ** 2 + (z - 16.1) ** 2)
+    ids, pos = MC.marching_cubes(np.clip(0.5 - 0.25 * (r - R), 0, 1))
+    n = _tri_normals(pos)
+    area = 0.5 * np.linalg.norm(n, axis=1).sum()
+    vol = np.einsum("ij,ij->i", pos[:, 0], n).sum() / 6
+    assert abs(area / (4 * math.pi * R * R) - 1) < 0.02
+    assert abs(vol / (4 / 3 * math.pi * R ** 3) - 1) < 0.02      # > 0: normals point outward
+    assert not _unpaired_directed_edges(ids)
+    V = len(set(ids.ravel().tolist()))
+    E = 3 * len(ids) // 2
+    assert V - E + len(ids) == 2
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_p16_random_fields_watertight_and_oriented(seed):
+    # every directed mesh edge meets its reverse exactly once (periodic x/y);
+    # only segments inside the bottom / top sample planes stay open.  Random
+    # fields hit the face-ambiguous configurations many times.
+    from oracle import mesh as MC
+    rng = np.random.default_rng(seed)
+    NX, NY, NZ = 9, 8, 7
+    phi = rng.random((NZ, NY, NX))
+    ids, pos = MC.marching_cubes(phi)
+    assert len(ids) > 100
+
+    def plane_of(e):
+        ax, lin = e % 3, e // 3
+        k = lin // (NX * NY)
+        return k if ax != 2 else -1
+
+    def skip(a, b):
+        pa, pb = plane_of(a), plane_of(b)
+        return pa == pb and pa in (0, NZ - 1)
+
+    assert not _unpaired_directed_edges(ids, skip)
+    # vertices: on their edge, where the linear interpolant equals iso
+    for tr, ps in zip(ids[:200], pos[:200]):
+        for e, p in zip(tr, ps):
+            ax, lin = e % 3, e // 3
+            lo = [lin % NX, (lin // NX) % NY, lin // (NX * NY)]
+            hi = list(lo)
+            hi[ax] += 1
+            f0 = phi[lo[2], lo[1], lo[0]]
+            f1 = phi[hi[2] % NZ, hi[1] % NY, hi[0] % NX]
+            t = p[ax] - (lo[ax] + 0.5)
+            assert 0 <= t <= 1 and abs(f0 + t * (f1 - f0) - 0.5) < 1e-12
+            for q in range(3):
+                if q != ax:
+                    assert p[q] == lo[q] + 0.5
+
+
+def test_p16_normals_point_down_the_gradient():
+    from oracle import mesh as MC
+    rng = np.random.default_rng(3)
+    N = 24
+    z, y, x = np.meshgrid(*(np.arange(N) + 0.5,) * 3, indexing="ij")
+    phi = 0.5 + 0.3 * np.sin(2 * np.pi * x / N) * np.cos(2 * np.pi * y / N) + 0.1 * np.sin(2 * np.pi * z / N + 0.3)
+    ids, pos = MC.marching_cubes(phi)
+    pos = _unwrap(pos, N, N)
+    c = pos.mean(axis=1)
+    gx = 0.3 * (2 * np.pi / N) * np.cos(2 * np.pi * c[:, 0] / N) * np.cos(2 * np.pi * c[:, 1] / N)
+    gy = -0.3 * (2 * np.pi / N) * np.sin(2 * np.pi * c[:, 0] / N) * np.sin(2 * np.pi * c[:, 1] / N)
+    gz = 0.1 * (2 * np.pi / N) * np.cos(2 * np.pi * c[:, 2] / N + 0.3)
+    dots = np.einsum("ij,ij->i", _tri_normals(pos), np.stack([gx, gy, gz], 1))
+    assert np.mean(dots < 0) > 0.99
+
+
+def test_p16_cube_cases_exhaustive():
+    # all 256 corner configurations: the triangle vertices are exactly the
+    # crossing edges, each triangle's edges lie in the cube, counts <= 5
+    from oracle import mesh as MC
+    for case in range(256):
+        ins = [(case >> c) & 1 == 1 for c in range(8)]
+        tris = MC.cube_triangles(ins)
+        cross = {e for e, (a, b, _) in enumerate(MC.EDGES) if ins[a] != ins[b]}
+        used = {e for t in tris for e in t}
+        assert used == cross, case
+        assert len(tris) <= 5
+        assert all(len(set(t)) == 3 for t in tris)
+        # the cube's patch is a surface with its boundary on the cube faces:
+        # a triangle side lying in a cube face is used once, any other side
+        # (a fan diagonal through the interior) exactly once in each direction
+        from collections import Counter
+        sides = Counter((t[s], t[(s + 1) % 3]) for t in tris for s in range(3))
+        for (a, b), n in sides.items():
+            on_face = any(set(MC.EDGES[a][:2]) | set(MC.EDGES[b][:2]) <= set(f) for f in MC.FACES)
+            assert n == 1 and (sides.get((b, a), 0) == (0 if on_face else 1)), (case, a, b)
