@@ -32,17 +32,21 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=(),
+          csrc: str | None = None) -> str:
+    """Compile libpf.so; `out`/`defines`/`csrc` build an alternative copy for A/B timing (tools/)."""
+    if out is None and not force and not needs_build():
         return LIB
+    src = csrc or CSRC
     inc, libdir = _nccl_dirs()
     cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
            "-I", inc, "-I", os.path.join(os.path.dirname(HERE), "include"),
-           "-o", LIB] + [os.path.join(CSRC, f) for f in SOURCES] + \
+           *[f"-D{d}" for d in defines],
+           "-o", out or LIB] + [os.path.join(src, f) for f in SOURCES] + \
           ["-L", libdir, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + libdir]
     subprocess.check_call(cmd)
-    return LIB
+    return out or LIB
 
 
 if __name__ == "__main__":

@@ -31,6 +31,7 @@ struct KParams {
   double g2[6];            // 2 gamma_ab per pair
   double gf4[6];           // 2 gamma_ab / (4 dx): isotropic face flux constant
   double g2m[NPH][NPH];    // 2 gamma_ab as a matrix (0 on the diagonal)
+  double g2mc[NPH][NPH];   // 2 gamma_ab / (2 dx)^2: isotropic Gram of raw centre differences
   double delta[6];         // cubic anisotropy per pair
   double om[NPH][NPH];     // 16/pi^2 gamma_ab (0 on the diagonal)
   double g3[NPH];          // triple coefficient of the triple excluding x
@@ -66,6 +67,7 @@ enum {
   T_MCHAT = 47,   // + a*2+c     m (as given; constant, kept for locality)
   T_DI2A = 55,    // + a*2+c     1/(2A^l) - 1/(2A^a), solids a < 3
   T_DCHAT = 61,   // + a*2+c     chat^l - chat^a,     solids a < 3
+  T_EPSTDX = 67,  // eps T / dx (the face-flux divergence factor)
   TAB = 68        // multiple of 4 doubles (32 B): rows stay aligned
 };
 static_assert(TAB % 4 == 0, "table row alignment");
@@ -164,7 +166,10 @@ __device__ __forceinline__ double cgrad(const KParams &kp, double lo, double hi)
 
 // Cell part of the phi update (oracle O4.1-4.11) given the cell value, its
 // chemical potential, centre gradients, the face-flux divergence sum_d (j^+ -
-// j^-) (before the 1/dx factor) and the plane's table row.
+// j^-) (before the 1/dx factor) and the plane's table row.  Isotropic runs
+// pass the raw centre differences phi(c+e) - phi(c-e) instead of the
+// gradients: there they only enter the Gram matrix, whose 1/(2dx)^2 is folded
+// into g2mc.
 __device__ __forceinline__ void phi_cell_update_div(const KParams &kp, const double *__restrict__ tab,
                                                     const double ph[NPH], const double mu[NMU],
                                                     const double gc[NPH][3], const double dsum[NPH],
@@ -189,23 +194,24 @@ __device__ __forceinline__ void phi_cell_update_div(const KParams &kp, const dou
   if (!kp.aniso) {
     // isotropic g = 2 gamma q: q_ab . grad_b = phi_a |grad_b|^2 - phi_b (grad_a . grad_b),
     // so dad_a = sum_b 2 gamma_ab (phi_a G_bb - phi_b G_ab) with the Gram matrix G
-    double Gm[NPH][NPH];
+    // of the centre differences (g2mc carries 2 gamma / (2 dx)^2)
+    double Gd[NPH], Go[6];
 #pragma unroll
-    for (int a = 0; a < NPH; ++a)
+    for (int a = 0; a < NPH; ++a) Gd[a] = gc[a][0] * gc[a][0] + gc[a][1] * gc[a][1] + gc[a][2] * gc[a][2];
 #pragma unroll
-      for (int b = a; b < NPH; ++b) {
-        Gm[a][b] = gc[a][0] * gc[b][0] + gc[a][1] * gc[b][1] + gc[a][2] * gc[b][2];
-        Gm[b][a] = Gm[a][b];
-      }
+    for (int p = 0; p < 6; ++p) {
+      const int a = pair_a(p), b = pair_b(p);
+      Go[p] = kp.g2mc[a][b] * (gc[a][0] * gc[b][0] + gc[a][1] * gc[b][1] + gc[a][2] * gc[b][2]);
+    }
 #pragma unroll
     for (int a = 0; a < NPH; ++a) {
       double wd = 0.0, wo = 0.0;
 #pragma unroll
       for (int b = 0; b < NPH; ++b) {
         if (b == a) continue;
-        const double g2 = kp.g2m[a][b];
-        wd += g2 * Gm[b][b];
-        wo += g2 * (ph[b] * Gm[a][b]);
+        const int p = a < b ? (a == 0 ? b - 1 : a + b) : (b == 0 ? a - 1 : a + b);   // pair index of {a,b}
+        wd += kp.g2mc[a][b] * Gd[b];
+        wo += ph[b] * Go[p];
       }
       dad[a] = ph[a] * wd - wo;
     }
@@ -239,12 +245,14 @@ __device__ __forceinline__ void phi_cell_update_div(const KParams &kp, const dou
   const double rS = 1.0 / S;
   const double pbar = rS * (ph[0] * ph[0] * ps[0] + ph[1] * ph[1] * ps[1] + ph[2] * ph[2] * ps[2] +
                             ph[3] * ph[3] * ps[3]);
-  const double epsT = tab[T_EPST], Teps = tab[T_TEPS];
+  const double epsT = tab[T_EPST], Teps = tab[T_TEPS], epsTdx = tab[T_EPSTDX];
+  double pp[6];   // pair products phi_b phi_e of the triple terms
+#pragma unroll
+  for (int p = 0; p < 6; ++p) pp[p] = ph[pair_a(p)] * ph[pair_b(p)];
+  const double rS2 = 2.0 * rS;
   double rhs[NPH], sum = 0.0;
 #pragma unroll
   for (int a = 0; a < NPH; ++a) {
-    // O4.6 divergence of the face fluxes
-    const double div = dsum[a] * kp.inv_dx;
     // O4.7 multi-obstacle derivative
     double om = 0.0;
 #pragma unroll
@@ -255,11 +263,12 @@ __device__ __forceinline__ void phi_cell_update_div(const KParams &kp, const dou
       int b = -1, e = -1;
 #pragma unroll
       for (int y = 0; y < NPH; ++y) if (y != a && y != x) { if (b < 0) b = y; else e = y; }
-      om += kp.g3[x] * ph[b] * ph[e];
+      om += kp.g3[x] * pp[b == 0 ? e - 1 : b + e];   // pair index of {b < e}
     }
     // O4.8 driving force
-    const double dpsi = 2.0 * ph[a] * rS * (ps[a] - pbar);
-    rhs[a] = epsT * (dad[a] - div) + Teps * om + dpsi;     // O4.9
+    const double dpsi = (ph[a] * rS2) * (ps[a] - pbar);
+    // O4.9 with the O4.6 divergence of the face fluxes (eps T / dx folded)
+    rhs[a] = (epsT * dad[a] - epsTdx * dsum[a]) + Teps * om + dpsi;
     sum += rhs[a];
   }
   const double mean = 0.25 * sum;

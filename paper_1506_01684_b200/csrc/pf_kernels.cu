@@ -21,6 +21,7 @@ __global__ void table_kernel(double *tab, int64_t nplanes, TabParams tp, int64_t
   row[T_T] = T;
   row[T_EPST] = tp.eps * T;
   row[T_TEPS] = T / tp.eps;
+  row[T_EPSTDX] = tp.eps * T / tp.dx;
   for (int a = 0; a < NPH; ++a) {
     row[T_B + a] = tp.L[a] * th / tp.T_eut;
     for (int c = 0; c < NMU; ++c) {
@@ -39,7 +40,6 @@ __global__ void table_kernel(double *tab, int64_t nplanes, TabParams tp, int64_t
       row[T_DI2A + a * 2 + c] = row[T_INV2A + LIQ * 2 + c] - row[T_INV2A + a * 2 + c];
       row[T_DCHAT + a * 2 + c] = row[T_CHAT + LIQ * 2 + c] - row[T_CHAT + a * 2 + c];
     }
-  row[TAB - 1] = 0.0;
 }
 
 void launch_table(cudaStream_t s, double *tab, int64_t nplanes, const TabParams &tp, int64_t step, int64_t zorig) {
@@ -79,6 +79,11 @@ __global__ void __launch_bounds__(128) phi_naive_kernel(KParams kp, BlockView b)
   mu[0] = __ldg(b.mu[0] + o);
   mu[1] = __ldg(b.mu[1] + o);
   centre_grads(kp, b.phi, o, st, gc);
+  double gcu[NPH][3];   // phi_cell_update: raw centre differences when isotropic
+#pragma unroll
+  for (int a = 0; a < NPH; ++a)
+#pragma unroll
+    for (int e = 0; e < 3; ++e) gcu[a][e] = kp.aniso ? gc[a][e] : __ldg(b.phi[a] + o + st[e]) - __ldg(b.phi[a] + o - st[e]);
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     double pl[NPH], pu[NPH], gl[NPH][3], gu[NPH][3];
@@ -91,7 +96,7 @@ __global__ void __launch_bounds__(128) phi_naive_kernel(KParams kp, BlockView b)
     phi_face(kp, pl, ph, gl, gc, d, jm[d]);
     phi_face(kp, ph, pu, gc, gu, d, jp[d]);
   }
-  phi_cell_update(kp, b.tab + (int64_t)k * TAB, ph, mu, gc, jm, jp, out);
+  phi_cell_update(kp, b.tab + (int64_t)k * TAB, ph, mu, gcu, jm, jp, out);
 #pragma unroll
   for (int a = 0; a < NPH; ++a) b.out[a][o] = out[a];
 }

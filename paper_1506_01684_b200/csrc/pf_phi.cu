@@ -202,9 +202,17 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) phi_tiled_kernel(const __gri
       double gc[NPH][3], dsum[NPH], mu[NMU], out[NPH];
 #pragma unroll
       for (int a = 0; a < NPH; ++a) {
-        gc[a][0] = cgrad(kp, T(S.p[sc][a], orow, oc - 1), T(S.p[sc][a], orow, oc + 1));
-        gc[a][1] = cgrad(kp, T(S.p[sc][a], orow - 1, oc), T(S.p[sc][a], orow + 1, oc));
-        gc[a][2] = cgrad(kp, pm[a], pp[a]);
+        // gradients (anisotropic) or raw centre differences (isotropic, see
+        // phi_cell_update_div)
+        if (ANISO) {
+          gc[a][0] = cgrad(kp, T(S.p[sc][a], orow, oc - 1), T(S.p[sc][a], orow, oc + 1));
+          gc[a][1] = cgrad(kp, T(S.p[sc][a], orow - 1, oc), T(S.p[sc][a], orow + 1, oc));
+          gc[a][2] = cgrad(kp, pm[a], pp[a]);
+        } else {
+          gc[a][0] = T(S.p[sc][a], orow, oc + 1) - T(S.p[sc][a], orow, oc - 1);
+          gc[a][1] = T(S.p[sc][a], orow + 1, oc) - T(S.p[sc][a], orow - 1, oc);
+          gc[a][2] = pp[a] - pm[a];
+        }
         dsum[a] = ((S.fx[fb][a][ty][tx + 1] - S.fx[fb][a][ty][tx]) + (S.fy[fb][a][ty + 1][tx] - S.fy[fb][a][ty][tx])) +
                   (jzp[a] - jzm[a]);
       }

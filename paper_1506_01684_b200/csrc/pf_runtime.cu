@@ -808,6 +808,7 @@ pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
     kp.g3[a] = p->gamma3[a];
     for (int b = 0; b < 4; ++b) kp.om[a][b] = a == b ? 0.0 : 16.0 / (M_PI * M_PI) * p->gamma[a][b];
     for (int b = 0; b < 4; ++b) kp.g2m[a][b] = a == b ? 0.0 : 2.0 * p->gamma[a][b];
+    for (int b = 0; b < 4; ++b) kp.g2mc[a][b] = kp.g2m[a][b] * kp.inv_2dx * kp.inv_2dx;
   }
   for (int q = 0; q < 6; ++q) {
     kp.g2[q] = 2.0 * p->gamma[pair_a(q)][pair_b(q)];

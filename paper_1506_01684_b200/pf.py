@@ -16,7 +16,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpf.so")
+# PF_LIB: an alternative build of the same library (A/B timing tools only)
+LIB_PATH = os.environ.get("PF_LIB") or os.path.join(_HERE, "libpf.so")
 
 D = ctypes.c_double
 I32 = ctypes.c_int32
