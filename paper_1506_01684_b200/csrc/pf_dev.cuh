@@ -343,11 +343,16 @@ __device__ __forceinline__ void mu_cell_q(const double *__restrict__ tab, const 
 // is evaluated as (pi eps/4) pb_a h_l pd (g_a . g_l) g_a,d / sqrt(pal |g_l|^2 |g_a|^4)
 // — one FP64 rsqrt per solid instead of three (algebraically identical; a
 // guarded fallback keeps it finite when the product leaves the normal range).
+// Diffusive part M grad mu of a face (arithmetic mean of the cell mobilities,
+// reading R11), pinned: the value every face starts from.
+__device__ __forceinline__ double mu_flux_diff(const KParams &kp, double Mlo, double Mhi, double mlo, double mhi) {
+  return RN_MUL(RN_MUL(RN_MUL(0.5, RN_ADD(Mlo, Mhi)), RN_SUB(mhi, mlo)), kp.inv_dx);
+}
+
 template <class QL, class QH>
 __device__ __forceinline__ void mu_face_t(const KParams &kp, const QL &lo, const QH &hi, int d, double out[NMU]) {
 #pragma unroll
-  for (int c = 0; c < NMU; ++c)
-    out[c] = RN_MUL(RN_MUL(RN_MUL(0.5, RN_ADD(lo.M(c), hi.M(c))), RN_SUB(hi.mu(c), lo.mu(c))), kp.inv_dx);
+  for (int c = 0; c < NMU; ++c) out[c] = mu_flux_diff(kp, lo.M(c), hi.M(c), lo.mu(c), hi.mu(c));
   const double pbl = RN_MUL(0.5, RN_ADD(lo.pn(LIQ), hi.pn(LIQ)));
   if (pbl == 0.0) return;                   // no liquid: J = 0 (bulk solid exits here)
   double gfl[3];

@@ -12,7 +12,11 @@
 //     face values of plane k.
 // Everything else a face needs (dphi, c^l - c^a, tangential gradients) is
 // derived from the staged planes inside the face routine, and only when the
-// exact-zero guards let the anti-trapping term through.  z-faces are carried
+// exact-zero guards let the anti-trapping term through.  Flat planes: when the
+// staged phi^{n+1}_l tiles make every guard of a plane's faces close (pure
+// liquid over planes k-1..k+1, or no liquid in the face cells), the CTA takes
+// the diffusive flux only — decided CTA-uniformly per plane from the staged
+// tiles, bitwise identical to the guarded path.  z-faces are carried
 // in registers; the own column's phi^n / mu at k+1 (the z-face's upper cell)
 // come from registers.  All arithmetic is the pinned code of pf_dev.cuh, so
 // results do not depend on tile or block boundaries.
@@ -32,7 +36,10 @@ struct __align__(128) MuSmem {
   double fy[NMU][TY + 1][TX];     // y-face values at j - 1/2
   uint64_t bar_pn[NSLOT];         // phi^{n+1} + table of a plane
   uint64_t bar_pm[2];             // phi^n + mu of a plane
+  uint32_t wflat[3][NTHR / 32];   // per-warp flatness votes of a staged phi^{n+1}_l plane
 };
+constexpr int NBOX = RX * RY;     // staged cells of a plane tile (interior + ring + corners)
+static_assert(NBOX <= 2 * NTHR, "flatness check covers the box in two passes");
 #define T(arr, row, col) TILE_AT(arr, row, col)
 constexpr uint32_t MU_PN_BYTES = (NPH * RXS * RY + TAB) * 8;   // phi^{n+1} tiles + table row
 constexpr uint32_t MU_PM_BYTES = ((NPH + NMU) * RXS * RY) * 8;  // phi^n + mu tiles
@@ -117,6 +124,29 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
 #pragma unroll
     for (int c = 0; c < NMU; ++c) tma_load_3d(S.mu[s][c], &tm.mu[c], bx, by, k + b.zoff, &S.bar_pm[s]);
   };
+  // flatness vote of the staged phi^{n+1}_l tile of plane k into wflat[e]:
+  // bit 0 = every cell is exactly 1 (pure liquid), bit 1 = every cell is 0
+  auto vote_flat = [&](int k, int e) {
+    const double *pl = S.pn[slot(k)][LIQ];
+    bool one = true, zero = true;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int q = tid + r * NTHR;
+      if (q < NBOX) {
+        const double v = TILE_AT(pl, q / RX, q % RX);
+        one = one && v == 1.0;
+        zero = zero && v == 0.0;
+      }
+    }
+    const uint32_t f = (__all_sync(0xffffffffu, one) ? 1u : 0u) | (__all_sync(0xffffffffu, zero) ? 2u : 0u);
+    if ((tid & 31) == 0) S.wflat[e][tid >> 5] = f;
+  };
+  auto read_flat = [&](int e) {
+    uint32_t f = 3u;
+#pragma unroll
+    for (int w = 0; w < NTHR / 32; ++w) f &= S.wflat[e][w];
+    return f;
+  };
   auto rawq = [&](int k, int col, int row) {
     return RawQ{S, kp, slot(k - 1), slot(k), slot(k + 1), slot2(k), col, row, S.tab[slot(k)], {0.0, 0.0}};
   };
@@ -168,7 +198,12 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
     own_q(k0 - 1, pom, mum, qm);
     own_q(k0, po_n, mu_n, qc);
     mu_face(kp, qm, qc, 2, fzm);
+    vote_flat(k0 - 1, 0);
+    vote_flat(k0, 1);
   }
+  __syncthreads();
+  uint32_t flm = read_flat(0), flc = read_flat(1), flp;   // flatness of planes k-1, k, k+1
+  int fe = 2;                                              // wflat entry of plane k+1
 
   for (int k = k0; k < k1; ++k) {
     const int sn = slot(k), s2 = slot2(k);
@@ -199,11 +234,39 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
         S.M[1][rrow][rcol] = mob_of(S.tab[sn], 1, po);
       }
     }
-    __syncthreads();  // C: M of plane k visible; faces of plane k-1 consumed
-    // phi^{n+1}(k+1), staged at A(k-1), first needed now
+    // phi^{n+1}(k+1), staged at A(k-1); its flatness vote
     if (k > k0) mbar_wait(&S.bar_pn[slot(k + 1)], par4(k + 1));
+    vote_flat(k + 1, fe);
+    __syncthreads();  // C: M of plane k and the votes visible; faces of plane k-1 consumed
+    flp = read_flat(fe);
+    fe = fe == 2 ? 0 : fe + 1;
+    // every x/y face of plane k has J = 0: liquid flat over k-1..k+1 (|grad phi_l|^2 = 0)
+    // or no liquid in plane k (phibar_l = 0); the z-face k+1/2 likewise over k, k+1
+    const bool fast_xy = ((flm & flc & flp) & 1u) || (flc & 2u);
+    const bool fast_z = ((flc & flp) & 1u) || ((flc & flp) & 2u);
+    flm = flc;
+    flc = flp;
     // D: faces of plane k
-    {
+    if (fast_xy) {
+#pragma unroll
+      for (int c = 0; c < NMU; ++c) {
+        const double mc = T(S.mu[s2][c], orow, oc), Mc = S.M[c][orow][oc];
+        S.fx[c][ty][tx] = mu_flux_diff(kp, S.M[c][orow][oc - 1], Mc, T(S.mu[s2][c], orow, oc - 1), mc);
+        S.fy[c][ty][tx] = mu_flux_diff(kp, S.M[c][orow - 1][oc], Mc, T(S.mu[s2][c], orow - 1, oc), mc);
+      }
+      if (tid < TX + TY) {
+        const int d = tid < TX ? 1 : 0;
+        const int c0 = d == 1 ? tid + 1 : TX, r0 = d == 1 ? TY : tid - TX + 1;
+        const int c1 = d == 1 ? c0 : c0 + 1, r1 = d == 1 ? r0 + 1 : r0;
+#pragma unroll
+        for (int c = 0; c < NMU; ++c) {
+          const double f = mu_flux_diff(kp, S.M[c][r0][c0], S.M[c][r1][c1], T(S.mu[s2][c], r0, c0),
+                                        T(S.mu[s2][c], r1, c1));
+          if (d == 0) S.fx[c][r0 - 1][TX] = f;
+          else S.fy[c][TY][c0 - 1] = f;
+        }
+      }
+    } else {
       double f[NMU];
       {  // own -x face
         RawQ lo = rawq(k, oc - 1, orow), hi = rawq(k, oc, orow);
@@ -234,8 +297,15 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
       }
     }
     double fzp[NMU], pn_c[NPH];
-    {  // z-face k+1/2: own cell at k (shared memory) and at k+1 (registers;
-       // the anti-trapping operands are only formed if the guards open)
+    if (fast_z) {
+      const int s1 = slot(k + 1);
+#pragma unroll
+      for (int c = 0; c < NMU; ++c)
+        fzp[c] = mu_flux_diff(kp, S.M[c][orow][oc], mob_of(S.tab[s1], c, po_n), T(S.mu[s2][c], orow, oc), mu_n[c]);
+#pragma unroll
+      for (int a = 0; a < NPH; ++a) pn_c[a] = T(S.pn[sn][a], orow, oc);
+    } else {  // z-face k+1/2: own cell at k (shared memory) and at k+1 (registers;
+              // the anti-trapping operands are only formed if the guards open)
       RawQ lo = rawq(k, oc, orow);
       lo.Mv[0] = S.M[0][orow][oc]; lo.Mv[1] = S.M[1][orow][oc];
       const int s1 = slot(k + 1);
