@@ -58,19 +58,25 @@ __device__ __forceinline__ bool is_vertex(const double p[NPH]) {
 // x-y slice).  TAB doubles per plane, index = global window plane + 1.
 enum {
   T_T = 0, T_EPST = 1, T_TEPS = 2,
-  T_INV2A = 3,    // + a*2 + c   1/(2A)
-  T_CHAT = 11,    // + a*2 + c   c-hat
-  T_INV4A = 19,   // + a*2 + c   1/(4A)
-  T_KAPPA = 27,   // + a*2 + c   2 A1 / (2A)^2
-  T_MC = 35,      // + a*2 + c   D / (2A)
-  T_B = 43,       // + a         L (T - T_eut) / T_eut
-  T_MCHAT = 47,   // + a*2+c     m (as given; constant, kept for locality)
-  T_DI2A = 55,    // + a*2+c     1/(2A^l) - 1/(2A^a), solids a < 3
-  T_DCHAT = 61,   // + a*2+c     chat^l - chat^a,     solids a < 3
-  T_EPSTDX = 67,  // eps T / dx (the face-flux divergence factor)
+  T_EPSTDX = 3,   // eps T / dx (the face-flux divergence factor)
+  // per (phase a, component c) pairs at base + a*2 + c; every base is even so
+  // the (c = 0, 1) pair of a phase is one 16-byte load (tab2)
+  T_INV2A = 4,    // 1/(2A)
+  T_CHAT = 12,    // c-hat
+  T_INV4A = 20,   // 1/(4A)
+  T_KAPPA = 28,   // 2 A1 / (2A)^2
+  T_MC = 36,      // D / (2A)
+  T_B = 44,       // + a         L (T - T_eut) / T_eut
+  T_MCHAT = 48,   // m (as given; constant, kept for locality)
+  T_DI2A = 56,    // 1/(2A^l) - 1/(2A^a), solids a < 3
+  T_DCHAT = 62,   // chat^l - chat^a,     solids a < 3
   TAB = 68        // multiple of 4 doubles (32 B): rows stay aligned
 };
 static_assert(TAB % 4 == 0, "table row alignment");
+// the (c = 0, 1) pair of phase a of a per-(phase, component) table entry
+__device__ __forceinline__ double2 tab2(const double *__restrict__ tab, int base, int a) {
+  return *reinterpret_cast<const double2 *>(tab + base + 2 * a);
+}
 
 #define RN_ADD __dadd_rn
 #define RN_SUB __dsub_rn
@@ -236,9 +242,10 @@ __device__ __forceinline__ void phi_cell_update_div(const KParams &kp, const dou
   double ps[NPH];
 #pragma unroll
   for (int a = 0; a < NPH; ++a) {
+    const double2 i4 = tab2(tab, T_INV4A, a), ch = tab2(tab, T_CHAT, a);
     double s = tab[T_B + a];
-#pragma unroll
-    for (int c = 0; c < NMU; ++c) s -= mu[c] * (mu[c] * tab[T_INV4A + a * 2 + c] + tab[T_CHAT + a * 2 + c]);
+    s -= mu[0] * (mu[0] * i4.x + ch.x);
+    s -= mu[1] * (mu[1] * i4.y + ch.y);
     ps[a] = s;
   }
   const double S = ph[0] * ph[0] + ph[1] * ph[1] + ph[2] * ph[2] + ph[3] * ph[3];
@@ -312,22 +319,27 @@ struct MuQ {
 __device__ __forceinline__ double dcl_of(const double *__restrict__ tab, int a, int c, double mu) {
   return RN_FMA(mu, tab[T_DI2A + a * 2 + c], tab[T_DCHAT + a * 2 + c]);
 }
-// mobility sum_a phi^n_a D/(2A) (pinned)
-__device__ __forceinline__ double mob_of(const double *__restrict__ tab, int c, const double po[NPH]) {
-  double M = RN_MUL(po[0], tab[T_MC + 0 * 2 + c]);
-  M = RN_FMA(po[1], tab[T_MC + 1 * 2 + c], M);
-  M = RN_FMA(po[2], tab[T_MC + 2 * 2 + c], M);
-  return RN_FMA(po[3], tab[T_MC + 3 * 2 + c], M);
+// mobility sum_a phi^n_a D/(2A) of both components (pinned)
+__device__ __forceinline__ void mob2(const double *__restrict__ tab, const double po[NPH], double M[NMU]) {
+  double2 m = tab2(tab, T_MC, 0);
+  M[0] = RN_MUL(po[0], m.x);
+  M[1] = RN_MUL(po[0], m.y);
+#pragma unroll
+  for (int a = 1; a < NPH; ++a) {
+    m = tab2(tab, T_MC, a);
+    M[0] = RN_FMA(po[a], m.x, M[0]);
+    M[1] = RN_FMA(po[a], m.y, M[1]);
+  }
 }
 
 __device__ __forceinline__ void mu_cell_q(const double *__restrict__ tab, const double po[NPH],
                                           const double pn[NPH], const double mu[NMU], MuQ &q) {
 #pragma unroll
   for (int a = 0; a < NPH; ++a) { q.pn[a] = pn[a]; q.dp[a] = RN_SUB(pn[a], po[a]); }
+  mob2(tab, po, q.M);
 #pragma unroll
   for (int c = 0; c < NMU; ++c) {
     q.mu[c] = mu[c];
-    q.M[c] = mob_of(tab, c, po);
 #pragma unroll
     for (int a = 0; a < 3; ++a) q.dcl[a][c] = dcl_of(tab, a, c, mu[c]);
   }
@@ -425,20 +437,20 @@ __device__ __forceinline__ void mu_cell_update(const KParams &kp, const double *
     hn[a] = pn[a] * pn[a] * rSn;
     dh[a] = hn[a] - po[a] * po[a] * rSo;
   }
-  double chi[NMU], rest[NMU];
+  double chi[NMU] = {0.0, 0.0}, s[NMU] = {0.0, 0.0}, dcdT[NMU] = {0.0, 0.0}, rest[NMU];
 #pragma unroll
-  for (int c = 0; c < NMU; ++c) {
-    double x = 0.0, s = 0.0, dcdT = 0.0;
-#pragma unroll
-    for (int a = 0; a < NPH; ++a) {
-      const double i2a = tab[T_INV2A + a * 2 + c];
-      x += hn[a] * i2a;                                                    // O5.3
-      s += (mu[c] * i2a + tab[T_CHAT + a * 2 + c]) * dh[a];                // O5.4 (sign below)
-      dcdT += hn[a] * (tab[T_MCHAT + a * 2 + c] - mu[c] * tab[T_KAPPA + a * 2 + c]);  // O5.5
-    }
-    chi[c] = x;
-    rest[c] = dcdT * kp.Gv - s * kp.inv_dt + divf[c] * kp.inv_dx;
+  for (int a = 0; a < NPH; ++a) {
+    const double2 i2a = tab2(tab, T_INV2A, a), ch = tab2(tab, T_CHAT, a);
+    const double2 mc = tab2(tab, T_MCHAT, a), ka = tab2(tab, T_KAPPA, a);
+    chi[0] += hn[a] * i2a.x;                                  // O5.3
+    chi[1] += hn[a] * i2a.y;
+    s[0] += (mu[0] * i2a.x + ch.x) * dh[a];                   // O5.4 (sign below)
+    s[1] += (mu[1] * i2a.y + ch.y) * dh[a];
+    dcdT[0] += hn[a] * (mc.x - mu[0] * ka.x);                 // O5.5
+    dcdT[1] += hn[a] * (mc.y - mu[1] * ka.y);
   }
+#pragma unroll
+  for (int c = 0; c < NMU; ++c) rest[c] = dcdT[c] * kp.Gv - s[c] * kp.inv_dt + divf[c] * kp.inv_dx;
   // mu^{n+1} = mu + dt/chi [ -s/dt + dcdT G v + div ]; one reciprocal for both chi
   const double rc = kp.dt / (chi[0] * chi[1]);
   out[0] = mu[0] + (chi[1] * rc) * rest[0];

@@ -126,14 +126,15 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
   };
   // flatness vote of the staged phi^{n+1}_l tile of plane k into wflat[e]:
   // bit 0 = every cell is exactly 1 (pure liquid), bit 1 = every cell is 0
+  const int vq0 = tid, vq1 = tid + NTHR;   // this thread's box cells (tile offsets)
+  const int vo[2] = {(vq0 / RX) * RXS + vq0 % RX + 1, (vq1 / RX) * RXS + vq1 % RX + 1};
   auto vote_flat = [&](int k, int e) {
     const double *pl = S.pn[slot(k)][LIQ];
     bool one = true, zero = true;
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
-      const int q = tid + r * NTHR;
-      if (q < NBOX) {
-        const double v = TILE_AT(pl, q / RX, q % RX);
+      if (tid + r * NTHR < NBOX) {
+        const double v = pl[vo[r]];
         one = one && v == 1.0;
         zero = zero && v == 0.0;
       }
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
     mbar_fence_init();
   }
   __syncthreads();
-  if (tid == 0) {
+  if (tid == ISSUER) {
     stage_pn(k0 - 1);
     stage_pn(k0);
     stage_pn(k0 + 1);
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
     const bool more = k + 1 < k1;
     // A: stage phi^{n+1}(k+2) and phi^n/mu(k+1) (their slots were last read in
     // D(k-1), before barrier E(k-1)); own column of plane k+1 into registers
-    if (tid == 0) {
+    if (tid == ISSUER) {
       if (k + 2 <= k1) stage_pn(k + 2);
       if (more) stage_pm(k + 1);
     }
@@ -225,13 +226,16 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
       double po[NPH];
 #pragma unroll
       for (int a = 0; a < NPH; ++a) po[a] = T(S.po[s2][a], orow, oc);
-      S.M[0][orow][oc] = mob_of(S.tab[sn], 0, po);
-      S.M[1][orow][oc] = mob_of(S.tab[sn], 1, po);
+      double M[NMU];
+      mob2(S.tab[sn], po, M);
+      S.M[0][orow][oc] = M[0];
+      S.M[1][orow][oc] = M[1];
       if (ring_thr && !rcorner) {
 #pragma unroll
         for (int a = 0; a < NPH; ++a) po[a] = T(S.po[s2][a], rrow, rcol);
-        S.M[0][rrow][rcol] = mob_of(S.tab[sn], 0, po);
-        S.M[1][rrow][rcol] = mob_of(S.tab[sn], 1, po);
+        mob2(S.tab[sn], po, M);
+        S.M[0][rrow][rcol] = M[0];
+        S.M[1][rrow][rcol] = M[1];
       }
     }
     // phi^{n+1}(k+1), staged at A(k-1); its flatness vote
@@ -298,10 +302,11 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
     }
     double fzp[NMU], pn_c[NPH];
     if (fast_z) {
-      const int s1 = slot(k + 1);
+      double Mn[NMU];
+      mob2(S.tab[slot(k + 1)], po_n, Mn);
 #pragma unroll
       for (int c = 0; c < NMU; ++c)
-        fzp[c] = mu_flux_diff(kp, S.M[c][orow][oc], mob_of(S.tab[s1], c, po_n), T(S.mu[s2][c], orow, oc), mu_n[c]);
+        fzp[c] = mu_flux_diff(kp, S.M[c][orow][oc], Mn[c], T(S.mu[s2][c], orow, oc), mu_n[c]);
 #pragma unroll
       for (int a = 0; a < NPH; ++a) pn_c[a] = T(S.pn[sn][a], orow, oc);
     } else {  // z-face k+1/2: own cell at k (shared memory) and at k+1 (registers;
@@ -309,8 +314,8 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
       RawQ lo = rawq(k, oc, orow);
       lo.Mv[0] = S.M[0][orow][oc]; lo.Mv[1] = S.M[1][orow][oc];
       const int s1 = slot(k + 1);
-      ColQ hi{S, kp, s1, oc, orow, S.tab[s1], po_n, mu_n,
-              {mob_of(S.tab[s1], 0, po_n), mob_of(S.tab[s1], 1, po_n)}};
+      ColQ hi{S, kp, s1, oc, orow, S.tab[s1], po_n, mu_n, {0.0, 0.0}};
+      mob2(S.tab[s1], po_n, hi.Mv);
       mu_face_t(kp, lo, hi, 2, fzp);
 #pragma unroll
       for (int a = 0; a < NPH; ++a) pn_c[a] = T(S.pn[sn][a], orow, oc);

@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) phi_tiled_kernel(const __gri
     mbar_fence_init();
   }
   __syncthreads();
-  if (tid == 0) {
+  if (tid == ISSUER) {
     stage(k0 - 1);
     stage(k0);
     stage(k0 + 1);
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) phi_tiled_kernel(const __gri
   for (int c = 0; c < NMU; ++c) mu_n[c] = active ? __ldg(b.mu[c] + (int64_t)k0 * b.plane + colo) : 0.0;
   for (int k = k0; k < k1; ++k) {
     // A: stage plane k+2 (needed from iteration k+1 on); wait for plane k+1
-    if (tid == 0 && k + 2 <= k1) stage(k + 2);
+    if (tid == ISSUER && k + 2 <= k1) stage(k + 2);
     double mu_c[NMU];
 #pragma unroll
     for (int c = 0; c < NMU; ++c) {

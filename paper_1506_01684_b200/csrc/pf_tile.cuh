@@ -20,6 +20,10 @@ constexpr int TX = TILE_X, TY = PF_TILE_Y, RX = TX + 2, RY = TY + 2;
 constexpr int NTHR = TX * TY;
 constexpr int NRING = 2 * RX + 2 * TY;  // 84 ring cells incl. the 4 in-plane corners
 constexpr int NSLOT = 4;                // plane slots: k-1, k, k+1 in use, k+2 in flight
+// the thread that issues the TMA copies: lane 0 of the last warp, which has no
+// far-face / ring work (warps 0-2 do), so the issue does not lengthen the
+// slowest warp's path to the next CTA barrier
+constexpr int ISSUER = NTHR - 32;
 
 // ring cell r -> (col, row) in the (RX x RY) tile (col/row 0 = index -1)
 __device__ __forceinline__ void ring_cell(int r, int &col, int &row) {
