@@ -176,10 +176,24 @@ __device__ __forceinline__ double cgrad(const KParams &kp, double lo, double hi)
 // pass the raw centre differences phi(c+e) - phi(c-e) instead of the
 // gradients: there they only enter the Gram matrix, whose 1/(2dx)^2 is folded
 // into g2mc.
+// Split in two so the tiled sweep can do everything that does not need the
+// face fluxes before its CTA barrier: phi_cell_rhs0 returns
+// r0_a = eps T da/dphi_a + (T/eps) domega/dphi_a + dpsi/dphi_a (O4.2-4.4,
+// 4.7-4.8), phi_cell_finish adds the divergence and does O4.9-4.11.
+__device__ __forceinline__ void phi_cell_rhs0(const KParams &kp, const double *__restrict__ tab,
+                                              const double ph[NPH], const double mu[NMU],
+                                              const double gc[NPH][3], double r0[NPH]);
+__device__ __forceinline__ void phi_cell_finish(const KParams &kp, const double *__restrict__ tab,
+                                                const double ph[NPH], const double r0[NPH],
+                                                const double dsum[NPH], double out[NPH]);
 __device__ __forceinline__ void phi_cell_update_div(const KParams &kp, const double *__restrict__ tab,
                                                     const double ph[NPH], const double mu[NMU],
                                                     const double gc[NPH][3], const double dsum[NPH],
-                                                    double out[NPH]);
+                                                    double out[NPH]) {
+  double r0[NPH];
+  phi_cell_rhs0(kp, tab, ph, mu, gc, r0);
+  phi_cell_finish(kp, tab, ph, r0, dsum, out);
+}
 
 __device__ __forceinline__ void phi_cell_update(const KParams &kp, const double *__restrict__ tab,
                                                 const double ph[NPH], const double mu[NMU],
@@ -191,10 +205,9 @@ __device__ __forceinline__ void phi_cell_update(const KParams &kp, const double 
   phi_cell_update_div(kp, tab, ph, mu, gc, dsum, out);
 }
 
-__device__ __forceinline__ void phi_cell_update_div(const KParams &kp, const double *__restrict__ tab,
-                                                    const double ph[NPH], const double mu[NMU],
-                                                    const double gc[NPH][3], const double dsum[NPH],
-                                                    double out[NPH]) {
+__device__ __forceinline__ void phi_cell_rhs0(const KParams &kp, const double *__restrict__ tab,
+                                              const double ph[NPH], const double mu[NMU],
+                                              const double gc[NPH][3], double r0[NPH]) {
   // d a / d phi_a = sum_{b != a} g_ab(q_ab) . grad phi_b   (O4.2-4)
   double dad[NPH] = {0.0, 0.0, 0.0, 0.0};
   if (!kp.aniso) {
@@ -252,12 +265,11 @@ __device__ __forceinline__ void phi_cell_update_div(const KParams &kp, const dou
   const double rS = 1.0 / S;
   const double pbar = rS * (ph[0] * ph[0] * ps[0] + ph[1] * ph[1] * ps[1] + ph[2] * ph[2] * ps[2] +
                             ph[3] * ph[3] * ps[3]);
-  const double epsT = tab[T_EPST], Teps = tab[T_TEPS], epsTdx = tab[T_EPSTDX];
+  const double epsT = tab[T_EPST], Teps = tab[T_TEPS];
   double pp[6];   // pair products phi_b phi_e of the triple terms
 #pragma unroll
   for (int p = 0; p < 6; ++p) pp[p] = ph[pair_a(p)] * ph[pair_b(p)];
   const double rS2 = 2.0 * rS;
-  double rhs[NPH], sum = 0.0;
 #pragma unroll
   for (int a = 0; a < NPH; ++a) {
     // O4.7 multi-obstacle derivative
@@ -274,8 +286,19 @@ __device__ __forceinline__ void phi_cell_update_div(const KParams &kp, const dou
     }
     // O4.8 driving force
     const double dpsi = (ph[a] * rS2) * (ps[a] - pbar);
-    // O4.9 with the O4.6 divergence of the face fluxes (eps T / dx folded)
-    rhs[a] = (epsT * dad[a] - epsTdx * dsum[a]) + Teps * om + dpsi;
+    r0[a] = epsT * dad[a] + Teps * om + dpsi;
+  }
+}
+
+__device__ __forceinline__ void phi_cell_finish(const KParams &kp, const double *__restrict__ tab,
+                                                const double ph[NPH], const double r0[NPH],
+                                                const double dsum[NPH], double out[NPH]) {
+  // O4.9 with the O4.6 divergence of the face fluxes (eps T / dx folded)
+  const double epsTdx = tab[T_EPSTDX];
+  double rhs[NPH], sum = 0.0;
+#pragma unroll
+  for (int a = 0; a < NPH; ++a) {
+    rhs[a] = r0[a] - epsTdx * dsum[a];
     sum += rhs[a];
   }
   const double mean = 0.25 * sum;

@@ -29,7 +29,10 @@ struct __align__(128) PhiSmem {
 constexpr uint32_t PHI_STAGE_BYTES = (NPH * RXS * RY + TAB) * 8;
 
 template <bool ANISO>
-__global__ void __launch_bounds__(NTHR, 512 / NTHR) phi_tiled_kernel(const __grid_constant__ TmaMaps tm, KParams kp, BlockView b,
+#ifndef PF_PHI_MINB
+#define PF_PHI_MINB (512 / NTHR)
+#endif
+__global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __grid_constant__ TmaMaps tm, KParams kp, BlockView b,
                                                             int kz) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   PhiSmem &S = *reinterpret_cast<PhiSmem *>(smem_raw);
@@ -172,12 +175,11 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) phi_tiled_kernel(const __gri
       }
       phi_face(kp, pc, pp, ANISO ? gl : gdum, ANISO ? gh : gdum, 2, jzp);
     }
-    __syncthreads();  // B: faces of plane k complete
     // region shortcut (NEXT-1): a warp whose cells
     // are all simplex vertices with an identical D3C7 (D3C19) neighbourhood
     // keeps phi^{n+1} = phi^n — bitwise what the full update returns (is_vertex)
-    bool skip = false;
-    if (kp.shortcuts) {
+    auto bulk_warp = [&]() {
+      if (!kp.shortcuts) return false;
       bool mine = is_vertex(pc);
 #pragma unroll
       for (int a = 0; a < NPH; ++a) {
@@ -192,33 +194,47 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) phi_tiled_kernel(const __gri
                  T(S.p[sp][a], orow, oc - 1) == v && T(S.p[sp][a], orow, oc + 1) == v &&
                  T(S.p[sp][a], orow - 1, oc) == v && T(S.p[sp][a], orow + 1, oc) == v;
       }
-      skip = __all_sync(0xffffffffu, mine || !active);
+      return __all_sync(0xffffffffu, mine || !active) != 0;
+    };
+    bool skip = ANISO ? false : bulk_warp();
+    // isotropic: the cell terms that need no face flux (phi_cell_rhs0, on the
+    // raw centre differences) are formed before the barrier, where the tile
+    // values are still in registers; the anisotropic kernel has no registers
+    // to spare for that and forms them after it
+    double r0[NPH];
+    if (!ANISO && active && !skip) {
+      double gc[NPH][3];
+#pragma unroll
+      for (int a = 0; a < NPH; ++a) {
+        gc[a][0] = T(S.p[sc][a], orow, oc + 1) - T(S.p[sc][a], orow, oc - 1);
+        gc[a][1] = T(S.p[sc][a], orow + 1, oc) - T(S.p[sc][a], orow - 1, oc);
+        gc[a][2] = pp[a] - pm[a];
+      }
+      phi_cell_rhs0(kp, S.tab[sc], pc, mu_c, gc, r0);
     }
+    __syncthreads();  // B: faces of plane k complete
+    if (ANISO) skip = bulk_warp();
     if (active && skip) {
       const int64_t o = (int64_t)k * b.plane + colo;
 #pragma unroll
       for (int a = 0; a < NPH; ++a) b.out[a][o] = pc[a];
     } else if (active) {
-      double gc[NPH][3], dsum[NPH], mu[NMU], out[NPH];
+      if (ANISO) {
+        double gc[NPH][3];
 #pragma unroll
-      for (int a = 0; a < NPH; ++a) {
-        // gradients (anisotropic) or raw centre differences (isotropic, see
-        // phi_cell_update_div)
-        if (ANISO) {
+        for (int a = 0; a < NPH; ++a) {
           gc[a][0] = cgrad(kp, T(S.p[sc][a], orow, oc - 1), T(S.p[sc][a], orow, oc + 1));
           gc[a][1] = cgrad(kp, T(S.p[sc][a], orow - 1, oc), T(S.p[sc][a], orow + 1, oc));
           gc[a][2] = cgrad(kp, pm[a], pp[a]);
-        } else {
-          gc[a][0] = T(S.p[sc][a], orow, oc + 1) - T(S.p[sc][a], orow, oc - 1);
-          gc[a][1] = T(S.p[sc][a], orow + 1, oc) - T(S.p[sc][a], orow - 1, oc);
-          gc[a][2] = pp[a] - pm[a];
         }
+        phi_cell_rhs0(kp, S.tab[sc], pc, mu_c, gc, r0);
+      }
+      double dsum[NPH], out[NPH];
+#pragma unroll
+      for (int a = 0; a < NPH; ++a)
         dsum[a] = ((S.fx[fb][a][ty][tx + 1] - S.fx[fb][a][ty][tx]) + (S.fy[fb][a][ty + 1][tx] - S.fy[fb][a][ty][tx])) +
                   (jzp[a] - jzm[a]);
-      }
-      mu[0] = mu_c[0];
-      mu[1] = mu_c[1];
-      phi_cell_update_div(kp, S.tab[sc], pc, mu, gc, dsum, out);
+      phi_cell_finish(kp, S.tab[sc], pc, r0, dsum, out);
       const int64_t o = (int64_t)k * b.plane + colo;
 #pragma unroll
       for (int a = 0; a < NPH; ++a) b.out[a][o] = out[a];
