@@ -190,6 +190,39 @@ pf_status pf_save(pf_ctx *c, const char *path);
  * PF_ERR_STATE until the next pf_init / pf_write / pf_load). */
 pf_status pf_load(pf_ctx *c, const char *path);
 
+/* Marching-cubes interface mesh of phase `phase` (0..3) over this rank's box
+ * ("a custom marching cubes algorithm ... generates meshes
+ * locally on each block, using the phi values as input.  For each phase, a
+ * mesh is generated ... extends to the ghost regions such that the local
+ * meshes can be stitched"; the variant is reading R26 of DESIGN.md §2).
+ *   Samples at cell centres; cube (i,j,k) has corners (i..i+1, j..j+1,
+ *   k..k+1), lower corner (global window index) in this rank's box, x/y
+ *   periodic, k <= NZ-2.  A corner is inside when phi > iso.  Cubes are taken
+ *   in (k, j, i) order, their triangles in case-table order: the output is
+ *   deterministic and identical to a serial sweep of the box.
+ *   ids [3*t + v]      int64 global grid-edge id of vertex v of triangle t:
+ *                      3*(i + NX*(j + NY*k)) + axis, (i,j,k) the edge's lower
+ *                      corner (x, y wrapped), axis 0/1/2 = x/y/z;
+ *   pos [9*t + 3*v + q] binary64 vertex position (x, y, z): ((g + 1/2) + s) dx
+ *                      along the edge, (g + 1/2) dx across it, g the global
+ *                      index (z from the window origin, plus z_origin), s =
+ *                      (iso - f0)/(f1 - f0) IEEE-rounded;
+ *   triangles are right-handed about the normal pointing out of the phase.
+ * At most `cap` triangles are written (cap = 0: count only; ids/pos may then
+ * be NULL); *ntri receives the total.  ids/pos are host or device pointers
+ * (auto-detected).  Collective only in the sense that every rank meshes its
+ * own box.  Errors: PF_ERR_STATE before pf_init/pf_write/pf_load, PF_ERR_ARG
+ * (phase out of range, NULL outputs with cap > 0, cap < 0), PF_ERR_CUDA. */
+pf_status pf_mesh(pf_ctx *c, int32_t phase, double iso, int64_t cap, int64_t *ids, double *pos, int64_t *ntri);
+
+/* Host-only query (no context, no GPU): the marching-cubes case table pf_mesh
+ * uses, out[16*case + 0] = triangle count (<= 5), out[16*case + 1 + 3*t + v] =
+ * cube edge of vertex v of triangle t (edges 0-3 along x at (dy,dz) =
+ * (e&1, e>>1), 4-7 along y at (dx,dz), 8-11 along z at (dx,dy); corner bit c
+ * = dx + 2dy + 4dz of `case` set when inside).  out: 256*16 int8 (caller
+ * owned).  Errors: PF_ERR_ARG on NULL. */
+pf_status pf_mesh_table(int8_t *out);
+
 /* Enable (1) / disable (0) per-sweep CUDA-event timing; resets the timers. */
 pf_status pf_set_timing(pf_ctx *c, int32_t on);
 

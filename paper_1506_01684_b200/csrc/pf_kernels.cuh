@@ -80,6 +80,13 @@ void launch_nancheck(cudaStream_t s, const double *const f[NPH], int ncomp, int 
 void launch_gather(cudaStream_t s, const double *const f[NPH], int ncomp, int nx, int ny, int nz, int64_t pitch,
                    int64_t plane, double *dst, int64_t dnx, int64_t dny, int64_t dn, int64_t ox, int64_t oy, int64_t oz,
                    bool scatter, double *const fw[NPH]);
+// marching-cubes case table {ntri, 3 edges per triangle} x 256 (host only)
+void mesh_case_table(int8_t *out);
+// marching-cubes mesh of one phase over the rank's box (pf_mesh.cu); synchronous
+cudaError_t launch_mesh(cudaStream_t s, const double *const *f, int bnx, int bny, int bnz, int pbx, int pby,
+                        int pbz, int64_t pitch, int64_t plane, int64_t nx, int64_t ny, int64_t nzc, int64_t X0,
+                        int64_t Y0, int64_t Z0, int64_t NX, int64_t NY, int64_t zorig, double iso, double dx,
+                        int64_t cap, int64_t *ids, double *pos, int64_t *ntri, void **scratch, size_t *scratch_bytes);
 void launch_cvt32(cudaStream_t s, double *f, int nx, int ny, int nz, int64_t pitch, int64_t plane, float *dst,
                   int64_t dnx, int64_t dny, int64_t ox, int64_t oy, int64_t oz, bool to_fields);
 

@@ -100,6 +100,12 @@ struct pf_ctx {
   int64_t launches = 0, phi_launches = 0, mu_launches = 0;
   // box of this rank
   int64_t box_nx = 0, box_ny = 0, box_nz = 0, box_x0 = 0, box_y0 = 0, box_z0 = 0;
+  // marching cubes (pf_mesh): block pointer table, scan scratch, host-output staging
+  const double **d_mesh_f = nullptr;
+  void *mesh_scratch = nullptr;
+  size_t mesh_scratch_bytes = 0;
+  void *mesh_out = nullptr;
+  size_t mesh_out_bytes = 0;
 };
 
 namespace {
@@ -1199,6 +1205,65 @@ const char *pf_last_error(const pf_ctx *c) {
   return c->err.c_str();
 }
 
+// Marching-cubes mesh of one phase over this rank's box (PAPER.md:246-251,
+// reading R26; kernels in pf_mesh.cu).  Cubes whose lower corner lies in the
+// box, the upper corners in the blocks' ghost layers ("extends to the ghost
+// regions"); in z only cubes below the global top plane (no cube reaches into
+// the zero-flux ghost), so the ranks' meshes together are the global mesh.
+pf_status pf_mesh(pf_ctx *c, int32_t phase, double iso, int64_t cap, int64_t *ids, double *pos, int64_t *ntri) {
+  CKS(check_state(c, true));
+  if (phase < 0 || phase >= NPH) return fail(c, PF_ERR_ARG, "phase %d out of range", (int)phase);
+  if (!ntri || cap < 0 || (cap > 0 && (!ids || !pos))) return fail(c, PF_ERR_ARG, "NULL output or negative cap");
+  CKS(join_mu(c));
+  const Block &b0 = c->blocks[0];
+  const int pbx = (int)(c->box_nx / b0.nx), pby = (int)(c->box_ny / b0.ny), pbz = (int)(c->box_nz / b0.nz);
+  // block pointers in box order (blocks of one rank are in block-id order)
+  std::vector<const double *> f(c->blocks.size());
+  for (const auto &b : c->blocks) {
+    const int q = (int)((b.x0 - c->box_x0) / b0.nx + pbx * ((b.y0 - c->box_y0) / b0.ny + pby * ((b.z0 - c->box_z0) / b0.nz)));
+    f[q] = field_ptr(b, 0, c->cur, phase) + cell_off(b, 0, 0, 0);
+  }
+  if (!c->d_mesh_f) CK(cudaMalloc(&c->d_mesh_f, f.size() * sizeof(double *)));
+  CK(cudaMemcpyAsync(c->d_mesh_f, f.data(), f.size() * sizeof(double *), cudaMemcpyHostToDevice, c->stream));
+  const int64_t nzc = std::min(c->box_nz, c->g.nz - 1 - c->box_z0);   // cube layers
+  const bool dev = cap > 0 && is_device_ptr(ids) && is_device_ptr(pos);
+  int64_t *d_ids = ids;
+  double *d_pos = pos;
+  if (cap > 0 && !dev) {  // host output: count first, then stage at most cap triangles
+    int64_t total = 0;
+    CK(launch_mesh(c->stream, c->d_mesh_f, b0.nx, b0.ny, b0.nz, pbx, pby, pbz, b0.pitch, b0.plane, c->box_nx,
+                   c->box_ny, nzc, c->box_x0, c->box_y0, c->box_z0, c->g.nx, c->g.ny, c->zorig, iso, c->p.dx, 0,
+                   nullptr, nullptr, &total, &c->mesh_scratch, &c->mesh_scratch_bytes));
+    const int64_t nt = std::min(total, cap);
+    const size_t need = (size_t)nt * (3 * sizeof(int64_t) + 9 * sizeof(double));
+    if (c->mesh_out_bytes < need) {
+      if (c->mesh_out) cudaFree(c->mesh_out);
+      c->mesh_out = nullptr;
+      c->mesh_out_bytes = 0;
+      CK(cudaMalloc(&c->mesh_out, need));
+      c->mesh_out_bytes = need;
+    }
+    d_ids = (int64_t *)c->mesh_out;
+    d_pos = (double *)(d_ids + 3 * nt);
+    cap = nt;
+  }
+  CK(launch_mesh(c->stream, c->d_mesh_f, b0.nx, b0.ny, b0.nz, pbx, pby, pbz, b0.pitch, b0.plane, c->box_nx, c->box_ny,
+                 nzc, c->box_x0, c->box_y0, c->box_z0, c->g.nx, c->g.ny, c->zorig, iso, c->p.dx, cap, d_ids, d_pos,
+                 ntri, &c->mesh_scratch, &c->mesh_scratch_bytes));
+  if (cap > 0 && !dev) {
+    CK(cudaMemcpy(ids, d_ids, (size_t)cap * 3 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(pos, d_pos, (size_t)cap * 9 * sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  c->launches += cap > 0 ? 2 : 1;
+  return PF_OK;
+}
+
+pf_status pf_mesh_table(int8_t *out) {
+  if (!out) return PF_ERR_ARG;
+  mesh_case_table(out);
+  return PF_OK;
+}
+
 void pf_destroy(pf_ctx *c) {
   if (!c) return;
   cudaSetDevice(c->g.device);
@@ -1220,6 +1285,9 @@ void pf_destroy(pf_ctx *c) {
   if (c->d_tab) cudaFree(c->d_tab);
   if (c->d_red) cudaFree(c->d_red);
   if (c->d_stage) cudaFree(c->d_stage);
+  if (c->d_mesh_f) cudaFree(c->d_mesh_f);
+  if (c->mesh_scratch) cudaFree(c->mesh_scratch);
+  if (c->mesh_out) cudaFree(c->mesh_out);
   for (auto e : c->ev) cudaEventDestroy(e);
   if (c->cstream) cudaStreamSynchronize(c->cstream);
   if (c->comm_mu) ncclCommDestroy(c->comm_mu);

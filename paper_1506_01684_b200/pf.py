@@ -28,7 +28,17 @@ PF_OK, PF_ERR_CONFIG, PF_ERR_NUMERICAL, PF_ERR_CUDA, PF_ERR_COMM, PF_ERR_STATE, 
 STATUS_NAMES = {0: "PF_OK", -1: "PF_ERR_CONFIG", -2: "PF_ERR_NUMERICAL", -3: "PF_ERR_CUDA", -4: "PF_ERR_COMM",
                 -5: "PF_ERR_STATE", -6: "PF_ERR_ARG", -7: "PF_ERR_IO"}
 EXPORTS = ["pf_nccl_unique_id", "pf_halo_plan", "pf_create", "pf_init", "pf_write", "pf_set_time", "pf_step", "pf_read",
-           "pf_save", "pf_load", "pf_set_timing", "pf_info", "pf_last_error", "pf_destroy"]
+           "pf_save", "pf_load", "pf_mesh", "pf_mesh_table", "pf_set_timing", "pf_info", "pf_last_error", "pf_destroy"]
+
+
+def mesh_table():
+    """The marching-cubes case table libpf.so generated (pf_mesh_table; host
+    only): int8[256, 16] = {ntri, then 3 cube-edge numbers per triangle}."""
+    t = np.zeros((256, 16), dtype=np.int8)
+    st = lib().pf_mesh_table(t.ctypes.data)
+    if st != PF_OK:
+        raise PfError(st, "pf_mesh_table")
+    return t
 
 
 class PfGrid(ctypes.Structure):
@@ -83,6 +93,8 @@ def lib():
         L.pf_read.argtypes = [vp, vp, vp]
         L.pf_save.argtypes = [vp, ctypes.c_char_p]
         L.pf_load.argtypes = [vp, ctypes.c_char_p]
+        L.pf_mesh.argtypes = [vp, I32, D, I64, vp, vp, ctypes.POINTER(I64)]
+        L.pf_mesh_table.argtypes = [vp]
         L.pf_set_timing.argtypes = [vp, I32]
         L.pf_info.argtypes = [vp, ctypes.POINTER(PfInfo)]
         L.pf_last_error.argtypes = [vp]
@@ -224,6 +236,17 @@ class Context:
     def load(self, path):
         """Restore a pf_save checkpoint (pf_load; collective)."""
         self._check(lib().pf_load(self._c, os.fsencode(path)))
+
+    def mesh(self, phase: int, iso: float = 0.5):
+        """Marching-cubes mesh of one phase over this rank's box (pf_mesh):
+        (ids int64[T, 3], pos float64[T, 3, 3])."""
+        n = I64(0)
+        self._check(lib().pf_mesh(self._c, phase, iso, 0, None, None, ctypes.byref(n)))
+        ids = np.empty((n.value, 3), dtype=np.int64)
+        pos = np.empty((n.value, 3, 3))
+        if n.value:
+            self._check(lib().pf_mesh(self._c, phase, iso, n.value, ids.ctypes.data, pos.ctypes.data, ctypes.byref(n)))
+        return ids, pos
 
     def set_timing(self, on: bool):
         self._check(lib().pf_set_timing(self._c, 1 if on else 0))

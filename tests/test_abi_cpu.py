@@ -53,3 +53,15 @@ def test_create_without_gpu_fails_loudly():
         assert e.status in (pf.PF_ERR_CUDA,)
     else:
         raise AssertionError("pf_create succeeded without a GPU")
+
+
+def test_mesh_case_table_matches_oracle():
+    # host logic of the CUDA path (pf_mesh_table, generated in C++ from reading
+    # R26) against the oracle's own case construction, all 256 cases
+    from paper_1506_01684_b200 import pf
+    from oracle import mesh as MC
+    t = pf.mesh_table()
+    for case in range(256):
+        ref = [tuple(tr) for tr in MC.cube_triangles([(case >> c) & 1 == 1 for c in range(8)])]
+        got = [tuple(int(x) for x in t[case, 1 + 3 * i:4 + 3 * i]) for i in range(t[case, 0])]
+        assert got == ref, case
