@@ -103,6 +103,18 @@ typedef struct {
                                  update, whose result is then its input bit for
                                  bit; results identical to shortcuts = 0         */
   double init_layer_height, init_iface_width, init_mu_noise;
+  int32_t overlap;            /* communication hiding:
+                                 0 (default): the mu^{n+1} halo exchange runs beside
+                                   the next phi-sweep (which reads mu at the cell
+                                   only) — the paper's best variant;
+                                 1: none (Algorithm 1 in order);
+                                 2: the phi^{n+1} halo exchange runs beside
+                                   mu-sweep-local (the mu update without the
+                                   anti-trapping current), then mu-sweep-neighbor
+                                   adds its divergence (Algorithm 2's split); the
+                                   mu halo is not hidden;
+                                 3: both (Algorithm 2).
+                                 Results of 2/3 differ from 0/1 by rounding only. */
 } pf_params;
 
 /* Run-time information about a context. */

@@ -384,10 +384,11 @@ __device__ __forceinline__ double mu_flux_diff(const KParams &kp, double Mlo, do
   return RN_MUL(RN_MUL(RN_MUL(0.5, RN_ADD(Mlo, Mhi)), RN_SUB(mhi, mlo)), kp.inv_dx);
 }
 
-template <class QL, class QH>
+// DIFF = false: the anti-trapping part -J alone (Algorithm 2's mu-sweep-neighbor).
+template <bool DIFF = true, class QL, class QH>
 __device__ __forceinline__ void mu_face_t(const KParams &kp, const QL &lo, const QH &hi, int d, double out[NMU]) {
 #pragma unroll
-  for (int c = 0; c < NMU; ++c) out[c] = mu_flux_diff(kp, lo.M(c), hi.M(c), lo.mu(c), hi.mu(c));
+  for (int c = 0; c < NMU; ++c) out[c] = DIFF ? mu_flux_diff(kp, lo.M(c), hi.M(c), lo.mu(c), hi.mu(c)) : 0.0;
   const double pbl = RN_MUL(0.5, RN_ADD(lo.pn(LIQ), hi.pn(LIQ)));
   if (pbl == 0.0) return;                   // no liquid: J = 0 (bulk solid exits here)
   double gfl[3];
@@ -478,6 +479,25 @@ __device__ __forceinline__ void mu_cell_update(const KParams &kp, const double *
   const double rc = kp.dt / (chi[0] * chi[1]);
   out[0] = mu[0] + (chi[1] * rc) * rest[0];
   out[1] = mu[1] + (chi[0] * rc) * rest[1];
+}
+
+// Algorithm 2's second half: add the anti-trapping
+// divergence divj = sum_d ((-J)^+ - (-J)^-) (before 1/dx) to the mu-sweep-local
+// result mu_loc, with the same chi(phi^{n+1}) as mu_cell_update.
+__device__ __forceinline__ void mu_cell_add_j(const KParams &kp, const double *__restrict__ tab, const double pn[NPH],
+                                              const double mu_loc[NMU], const double divj[NMU], double out[NMU]) {
+  const double rSn = 1.0 / (pn[0] * pn[0] + pn[1] * pn[1] + pn[2] * pn[2] + pn[3] * pn[3]);
+  double chi[NMU] = {0.0, 0.0};
+#pragma unroll
+  for (int a = 0; a < NPH; ++a) {
+    const double hn = pn[a] * pn[a] * rSn;
+    const double2 i2a = tab2(tab, T_INV2A, a);
+    chi[0] += hn * i2a.x;
+    chi[1] += hn * i2a.y;
+  }
+  const double rc = kp.dt / (chi[0] * chi[1]);
+  out[0] = mu_loc[0] + (chi[1] * rc) * (divj[0] * kp.inv_dx);
+  out[1] = mu_loc[1] + (chi[0] * rc) * (divj[1] * kp.inv_dx);
 }
 
 }  // namespace pf

@@ -159,23 +159,30 @@ void launch_mu_naive(cudaStream_t s, const KParams &kp, const BlockView &b) {
 // Halo: strided 3D box copies (local copy, pack into / unpack from NCCL
 // buffers).  blockIdx.y = op index.
 // ---------------------------------------------------------------------------
-__global__ void copy_kernel(const CopyOp *__restrict__ ops, int64_t max_cells) {
-  const CopyOp op = ops[blockIdx.y];
-  const int64_t n = (int64_t)op.ex * op.ey * op.ez;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t x = t % op.ex, y = (t / op.ex) % op.ey, z = t / ((int64_t)op.ex * op.ey);
+// One launch copies a list of boxes; op q owns CTAs [cta0_q, cta0_{q+1}),
+// each CTA 1024 cells of it.  A box is at most a face of a block (< 2^32
+// cells), so the index split uses 32-bit division.
+__global__ void copy_kernel(const CopyOp *__restrict__ ops, int nops) {
+  int q = 0;
+  while (q + 1 < nops && __ldg(&ops[q + 1].cta0) <= (int64_t)blockIdx.x) ++q;
+  const CopyOp op = ops[q];
+  const uint32_t ex = (uint32_t)op.ex, ey = (uint32_t)op.ey;
+  const uint32_t n = ex * ey * (uint32_t)op.ez;
+  const uint32_t base = (uint32_t)(blockIdx.x - op.cta0) * COPY_CELLS_PER_CTA;
+#pragma unroll
+  for (int e = 0; e < COPY_CELLS_PER_CTA / 256; ++e) {
+    const uint32_t t = base + e * 256 + threadIdx.x;
+    if (t >= n) break;
+    const uint32_t r = t / ex, x = t - r * ex, z = r / ey, y = r - z * ey;
     const int64_t so = x * op.ssx + y * op.ssy + z * op.ssz;
     const int64_t dof = x * op.dsx + y * op.dsy + z * op.dsz;
     for (int c = 0; c < op.ncomp; ++c) op.dst[c][dof] = op.src[c][so];
   }
 }
 
-void launch_copy(cudaStream_t s, const CopyOp *d_ops, int nops, int64_t max_cells) {
-  if (nops <= 0) return;
-  int64_t bx = (max_cells + 255) / 256;
-  if (bx > 1184) bx = 1184;
-  if (bx < 1) bx = 1;
-  copy_kernel<<<dim3((unsigned)bx, (unsigned)nops), 256, 0, s>>>(d_ops, max_cells);
+void launch_copy(cudaStream_t s, const CopyOp *d_ops, int nops, int64_t nctas) {
+  if (nops <= 0 || nctas <= 0) return;
+  copy_kernel<<<(unsigned)nctas, 256, 0, s>>>(d_ops, nops);
 }
 
 // ---------------------------------------------------------------------------

@@ -45,7 +45,9 @@ struct CopyOp {
   int64_t dsx, dsy, dsz;    // destination strides
   int ex, ey, ez;           // extents
   int ncomp;
+  int64_t cta0;             // first CTA of this op in its launch (upload_ops)
 };
+constexpr int COPY_CELLS_PER_CTA = 1024;   // 256 threads x 4 cells
 
 struct InitSpec {
   int kind, n_seeds, nlam;
@@ -67,8 +69,12 @@ void launch_table(cudaStream_t s, double *tab, int64_t nplanes, const TabParams 
 void launch_phi_naive(cudaStream_t s, const KParams &kp, const BlockView &b);
 void launch_mu_naive(cudaStream_t s, const KParams &kp, const BlockView &b);
 void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm);
-void launch_mu_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm);
-void launch_copy(cudaStream_t s, const CopyOp *d_ops, int nops, int64_t max_cells);
+// mu-sweep modes: the whole update (Algorithm 1), or Algorithm 2's split
+// into the part without the anti-trapping current and the
+// part that adds its divergence after the phi^{n+1} halo exchange
+enum { MU_FULL = 0, MU_LOCAL = 1, MU_NEIGHBOR = 2 };
+void launch_mu_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm, int mode = MU_FULL);
+void launch_copy(cudaStream_t s, const CopyOp *d_ops, int nops, int64_t nctas);
 void launch_init(cudaStream_t s, const InitSpec &is, double *const phi[NPH], double *const mu[NMU],
                  int nx, int ny, int nz, int64_t pitch, int64_t plane, int64_t x0, int64_t y0, int64_t z0);
 void launch_fill_plane(cudaStream_t s, double *const f[NPH], int ncomp, const double *vals, int nx, int ny,

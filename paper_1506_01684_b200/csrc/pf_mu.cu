@@ -86,6 +86,11 @@ struct ColQ {
   __device__ __forceinline__ double dcl(int a, int c) const { return dcl_of(tab, a, c, muv[c]); }
 };
 
+// MODE: MU_FULL the whole mu update (Algorithm 1); MU_LOCAL everything but the
+// anti-trapping current, MU_NEIGHBOR only its divergence added to the
+// MU_LOCAL result (Algorithm 2: the local part needs no
+// phi^{n+1} ghosts, so the phi halo exchange can run beside it).
+template <int MODE>
 __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid_constant__ TmaMaps tm, KParams kp,
                                                            BlockView b, int kz) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -198,7 +203,12 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
     MuQ qm, qc;
     own_q(k0 - 1, pom, mum, qm);
     own_q(k0, po_n, mu_n, qc);
-    mu_face(kp, qm, qc, 2, fzm);
+    if (MODE == MU_LOCAL) {
+#pragma unroll
+      for (int c = 0; c < NMU; ++c) fzm[c] = mu_flux_diff(kp, qm.M[c], qc.M[c], qm.mu[c], qc.mu[c]);
+    } else {
+      mu_face_t<MODE == MU_FULL>(kp, MuQAcc{qm}, MuQAcc{qc}, 2, fzm);
+    }
     vote_flat(k0 - 1, 0);
     vote_flat(k0, 1);
   }
@@ -222,7 +232,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
     for (int c = 0; c < NMU; ++c) mu_c[c] = mu_n[c];
     own_load(k + 1, po_n, mu_n);
     mbar_wait(&S.bar_pm[s2], par2(k));   // phi^n / mu of plane k resident
-    {  // mobility of plane k (own + ring cells)
+    if (MODE != MU_NEIGHBOR) {  // mobility of plane k (own + ring cells)
       double po[NPH];
 #pragma unroll
       for (int a = 0; a < NPH; ++a) po[a] = T(S.po[s2][a], orow, oc);
@@ -246,12 +256,25 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
     fe = fe == 2 ? 0 : fe + 1;
     // every x/y face of plane k has J = 0: liquid flat over k-1..k+1 (|grad phi_l|^2 = 0)
     // or no liquid in plane k (phibar_l = 0); the z-face k+1/2 likewise over k, k+1
-    const bool fast_xy = ((flm & flc & flp) & 1u) || (flc & 2u);
-    const bool fast_z = ((flc & flp) & 1u) || ((flc & flp) & 2u);
+    const bool fast_xy = MODE == MU_LOCAL || ((flm & flc & flp) & 1u) || (flc & 2u);
+    const bool fast_z = MODE == MU_LOCAL || ((flc & flp) & 1u) || ((flc & flp) & 2u);
     flm = flc;
     flc = flp;
     // D: faces of plane k
-    if (fast_xy) {
+    if (fast_xy && MODE == MU_NEIGHBOR) {   // J = 0 on every x/y face of the plane
+#pragma unroll
+      for (int c = 0; c < NMU; ++c) {
+        S.fx[c][ty][tx] = 0.0;
+        S.fy[c][ty][tx] = 0.0;
+      }
+      if (tid < TX + TY) {
+#pragma unroll
+        for (int c = 0; c < NMU; ++c) {
+          if (tid >= TX) S.fx[c][tid - TX][TX] = 0.0;
+          else S.fy[c][TY][tid] = 0.0;
+        }
+      }
+    } else if (fast_xy) {
 #pragma unroll
       for (int c = 0; c < NMU; ++c) {
         const double mc = T(S.mu[s2][c], orow, oc), Mc = S.M[c][orow][oc];
@@ -276,7 +299,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
         RawQ lo = rawq(k, oc - 1, orow), hi = rawq(k, oc, orow);
         lo.Mv[0] = S.M[0][orow][oc - 1]; lo.Mv[1] = S.M[1][orow][oc - 1];
         hi.Mv[0] = S.M[0][orow][oc]; hi.Mv[1] = S.M[1][orow][oc];
-        mu_face_t(kp, lo, hi, 0, f);
+        mu_face_t<MODE == MU_FULL>(kp, lo, hi, 0, f);
         S.fx[0][ty][tx] = f[0];
         S.fx[1][ty][tx] = f[1];
       }
@@ -284,7 +307,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
         RawQ lo = rawq(k, oc, orow - 1), hi = rawq(k, oc, orow);
         lo.Mv[0] = S.M[0][orow - 1][oc]; lo.Mv[1] = S.M[1][orow - 1][oc];
         hi.Mv[0] = S.M[0][orow][oc]; hi.Mv[1] = S.M[1][orow][oc];
-        mu_face_t(kp, lo, hi, 1, f);
+        mu_face_t<MODE == MU_FULL>(kp, lo, hi, 1, f);
         S.fy[0][ty][tx] = f[0];
         S.fy[1][ty][tx] = f[1];
       }
@@ -295,13 +318,17 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
         RawQ lo = rawq(k, c0, r0), hi = rawq(k, c1, r1);
         lo.Mv[0] = S.M[0][r0][c0]; lo.Mv[1] = S.M[1][r0][c0];
         hi.Mv[0] = S.M[0][r1][c1]; hi.Mv[1] = S.M[1][r1][c1];
-        mu_face_t(kp, lo, hi, d, f);
+        mu_face_t<MODE == MU_FULL>(kp, lo, hi, d, f);
         if (d == 0) { S.fx[0][r0 - 1][TX] = f[0]; S.fx[1][r0 - 1][TX] = f[1]; }
         else { S.fy[0][TY][c0 - 1] = f[0]; S.fy[1][TY][c0 - 1] = f[1]; }
       }
     }
     double fzp[NMU], pn_c[NPH];
-    if (fast_z) {
+    if (fast_z && MODE == MU_NEIGHBOR) {
+      fzp[0] = fzp[1] = 0.0;
+#pragma unroll
+      for (int a = 0; a < NPH; ++a) pn_c[a] = T(S.pn[sn][a], orow, oc);
+    } else if (fast_z) {
       double Mn[NMU];
       mob2(S.tab[slot(k + 1)], po_n, Mn);
 #pragma unroll
@@ -315,8 +342,8 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
       lo.Mv[0] = S.M[0][orow][oc]; lo.Mv[1] = S.M[1][orow][oc];
       const int s1 = slot(k + 1);
       ColQ hi{S, kp, s1, oc, orow, S.tab[s1], po_n, mu_n, {0.0, 0.0}};
-      mob2(S.tab[s1], po_n, hi.Mv);
-      mu_face_t(kp, lo, hi, 2, fzp);
+      if (MODE == MU_FULL) mob2(S.tab[s1], po_n, hi.Mv);
+      mu_face_t<MODE == MU_FULL>(kp, lo, hi, 2, fzp);
 #pragma unroll
       for (int a = 0; a < NPH; ++a) pn_c[a] = T(S.pn[sn][a], orow, oc);
     }
@@ -328,10 +355,17 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
       for (int c = 0; c < NMU; ++c)
         divf[c] = ((S.fx[c][ty][tx + 1] - S.fx[c][ty][tx]) + (S.fy[c][ty + 1][tx] - S.fy[c][ty][tx])) +
                   (fzp[c] - fzm[c]);
-      mu_cell_update(kp, S.tab[sn], po_c, pn_c, mu_c, divf, out);
       const int64_t o = (int64_t)k * b.plane + colo;
-      b.out[0][o] = out[0];
-      b.out[1][o] = out[1];
+      if (MODE != MU_NEIGHBOR) {
+        mu_cell_update(kp, S.tab[sn], po_c, pn_c, mu_c, divf, out);
+        b.out[0][o] = out[0];
+        b.out[1][o] = out[1];
+      } else if (divf[0] != 0.0 || divf[1] != 0.0) {   // divj = 0: mu_loc stands, bit for bit
+        const double loc[NMU] = {b.out[0][o], b.out[1][o]};
+        mu_cell_add_j(kp, S.tab[sn], pn_c, loc, divf, out);
+        b.out[0][o] = out[0];
+        b.out[1][o] = out[1];
+      }
     }
     fzm[0] = fzp[0];
     fzm[1] = fzp[1];
@@ -339,14 +373,21 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
 #undef T
 }
 
-void launch_mu_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm) {
+template <int MODE>
+void launch_mu_mode(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm) {
   const int gx = (b.nx + TX - 1) / TX, gy = (b.ny + TY - 1) / TY;
   const int kz = chunk_z(b.nz, gx * gy);
   dim3 grd(gx, gy, (b.nz + kz - 1) / kz), blk(TX, TY);
   const size_t sm = sizeof(MuSmem);
   static bool attr = false;
-  if (!attr) { cudaFuncSetAttribute(mu_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr = true; }
-  mu_tiled_kernel<<<grd, blk, sm, s>>>(tm, kp, b, kz);
+  if (!attr) { cudaFuncSetAttribute(mu_tiled_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr = true; }
+  mu_tiled_kernel<MODE><<<grd, blk, sm, s>>>(tm, kp, b, kz);
+}
+
+void launch_mu_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm, int mode) {
+  if (mode == MU_LOCAL) launch_mu_mode<MU_LOCAL>(s, kp, b, tm);
+  else if (mode == MU_NEIGHBOR) launch_mu_mode<MU_NEIGHBOR>(s, kp, b, tm);
+  else launch_mu_mode<MU_FULL>(s, kp, b, tm);
 }
 
 }  // namespace pf

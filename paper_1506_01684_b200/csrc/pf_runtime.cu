@@ -49,7 +49,7 @@ struct Block {
 struct Plan {                // halo plan of one field in one copy
   CopyOp *d_local = nullptr, *d_pack = nullptr, *d_unpack = nullptr;
   int nlocal = 0, npack = 0, nunpack = 0;
-  int64_t max_local = 0, max_pack = 0, max_unpack = 0;
+  int64_t max_local = 0, max_pack = 0, max_unpack = 0;   // after upload: CTAs of the local / unpack launches
 };
 
 struct Peer {
@@ -73,6 +73,7 @@ struct pf_ctx {
   // cstream (with its own communicator) while the next phi-sweep runs on stream
   cudaStream_t cstream = nullptr;
   cudaEvent_t ev_mu_done = nullptr, ev_mu_halo = nullptr;
+  cudaEvent_t ev_phi_done = nullptr, ev_phi_halo = nullptr;   // Algorithm 2's phi halo hiding
   bool mu_pending = false;
   ncclComm_t comm_mu = nullptr;
   double *d_tab = nullptr;
@@ -200,9 +201,17 @@ int local_index(const pf_ctx *c, int bid) {
   return -1;
 }
 
-pf_status upload_ops(pf_ctx *c, const std::vector<CopyOp> &ops, CopyOp **d) {
+// Upload a copy list; each op gets CTAs in proportion to its size (first CTA
+// in cta0), *nctas = the launch's CTA count: a 12-edge + 6-face halo is then a
+// few thousand CTAs, not 18 x the largest face's.
+pf_status upload_ops(pf_ctx *c, std::vector<CopyOp> ops, CopyOp **d, int64_t *nctas) {
   if (*d) { cudaFree(*d); *d = nullptr; }
+  *nctas = 0;
   if (ops.empty()) return PF_OK;
+  for (auto &op : ops) {
+    op.cta0 = *nctas;
+    *nctas += ((int64_t)op.ex * op.ey * op.ez + COPY_CELLS_PER_CTA - 1) / COPY_CELLS_PER_CTA;
+  }
   CK(cudaMalloc(d, ops.size() * sizeof(CopyOp)));
   CK(cudaMemcpy(*d, ops.data(), ops.size() * sizeof(CopyOp), cudaMemcpyHostToDevice));
   return PF_OK;
@@ -374,9 +383,9 @@ pf_status build_plans(pf_ctx *c) {
       first.insert(first.end(), local.begin(), local.end());
       pl.nlocal = (int)first.size();
       pl.max_local = std::max(pl.max_local, pl.max_pack);
-      CKS(upload_ops(c, first, &pl.d_local));
+      CKS(upload_ops(c, first, &pl.d_local, &pl.max_local));
       pl.nunpack = (int)unpack.size();
-      CKS(upload_ops(c, unpack, &pl.d_unpack));
+      CKS(upload_ops(c, unpack, &pl.d_unpack, &pl.max_unpack));
     }
   }
   return PF_OK;
@@ -744,6 +753,7 @@ pf_status validate(const pf_grid *g, const pf_params *p) {
         if (!(p->A0[a][q] + p->A1[a][q] * (T - p->T_eut) > 0))
           return fail(c, PF_ERR_CONFIG, "A[%d][%d](T=%g) <= 0", a, q, T);
   if (p->window && !(p->window_frac > 0 && p->window_frac <= 1)) return fail(c, PF_ERR_CONFIG, "window_frac");
+  if (p->overlap < 0 || p->overlap > 3) return fail(c, PF_ERR_CONFIG, "overlap must be 0..3");
   return PF_OK;
 }
 
@@ -881,7 +891,9 @@ pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
   }
   if (cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_mu_done, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_mu_halo, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&c->ev_mu_halo, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_phi_done, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_phi_halo, cudaEventDisableTiming) != cudaSuccess) {
     fail(c, PF_ERR_CUDA, "comm stream / events");
     return bail(PF_ERR_CUDA);
   }
@@ -1014,26 +1026,48 @@ pf_status pf_step(pf_ctx *c, int64_t n) {
       }
     }
     CK(cudaGetLastError());
-    CKS(exchange(c, 0, c->cur ^ 1));    // lines 2-3: phi_dst ghosts + boundary
-    CKS(join_mu(c));                    // mu_src ghosts (previous step's overlapped exchange)
-    {  // mu-sweep (line 4)
+    const int ov = c->p.overlap;
+    const bool hide_phi = (ov == 2 || ov == 3) && c->p.variant != 1, hide_mu = ov == 0 || ov == 3;
+    auto mu_sweep = [&](int mode) -> pf_status {
       TimedSpan ts(c, 1, (int)c->blocks.size());
       for (const auto &b : c->blocks) {
         const BlockView v = view(c, b, 1);
         if (c->p.variant == 1) launch_mu_naive(c->stream, c->kp, v);
-        else launch_mu_tiled(c->stream, c->kp, v, maps_of(c, b, 1));
+        else launch_mu_tiled(c->stream, c->kp, v, maps_of(c, b, 1), mode);
         c->launches++;
       }
+      CK(cudaGetLastError());
+      return PF_OK;
+    };
+    if (hide_phi) {
+      // Algorithm 2: phi_dst ghosts on the comm stream while
+      // mu-sweep-local (no anti-trapping current: phi_dst needed at the cell
+      // only) runs; mu-sweep-neighbor adds the current once the ghosts are in
+      CK(cudaEventRecord(c->ev_phi_done, c->stream));
+      CK(cudaStreamWaitEvent(c->cstream, c->ev_phi_done, 0));
+      CKS(exchange(c, 0, c->cur ^ 1, true));
+      CK(cudaEventRecord(c->ev_phi_halo, c->cstream));
+      CKS(join_mu(c));                  // mu_src ghosts (previous step's exchange)
+      CKS(mu_sweep(MU_LOCAL));
+      CK(cudaStreamWaitEvent(c->stream, c->ev_phi_halo, 0));
+      CKS(mu_sweep(MU_NEIGHBOR));
+    } else {
+      CKS(exchange(c, 0, c->cur ^ 1));  // lines 2-3: phi_dst ghosts + boundary
+      CKS(join_mu(c));                  // mu_src ghosts (previous step's overlapped exchange)
+      CKS(mu_sweep(MU_FULL));           // line 4
     }
-    CK(cudaGetLastError());
     // lines 5-6: mu_dst ghosts + boundary.  The next phi-sweep reads mu at the
-    // cell centre only (D3C1), so this exchange overlaps it
-    // on the comm stream (Algorithm 2's mu communication hiding)
-    CK(cudaEventRecord(c->ev_mu_done, c->stream));
-    CK(cudaStreamWaitEvent(c->cstream, c->ev_mu_done, 0));
-    CKS(exchange(c, 1, c->cur ^ 1, true));
-    CK(cudaEventRecord(c->ev_mu_halo, c->cstream));
-    c->mu_pending = true;
+    // cell centre only (D3C1), so this exchange can overlap
+    // it on the comm stream (the paper's mu communication hiding)
+    if (hide_mu) {
+      CK(cudaEventRecord(c->ev_mu_done, c->stream));
+      CK(cudaStreamWaitEvent(c->cstream, c->ev_mu_done, 0));
+      CKS(exchange(c, 1, c->cur ^ 1, true));
+      CK(cudaEventRecord(c->ev_mu_halo, c->cstream));
+      c->mu_pending = true;
+    } else {
+      CKS(exchange(c, 1, c->cur ^ 1));
+    }
     c->cur ^= 1;                        // line 7: swap
     c->step += 1;
     const bool nan_due = c->p.nan_check_every > 0 && c->step % c->p.nan_check_every == 0;
@@ -1294,6 +1328,8 @@ void pf_destroy(pf_ctx *c) {
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->ev_mu_done) cudaEventDestroy(c->ev_mu_done);
   if (c->ev_mu_halo) cudaEventDestroy(c->ev_mu_halo);
+  if (c->ev_phi_done) cudaEventDestroy(c->ev_phi_done);
+  if (c->ev_phi_halo) cudaEventDestroy(c->ev_phi_halo);
   if (c->cstream) cudaStreamDestroy(c->cstream);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   cudaGetLastError();
