@@ -290,3 +290,40 @@ def test_shortcuts_bitwise_aniso_window_blocks(pv1):
     a = _run_variant(pd, cfg, phi, mu, 120, False, **kw)
     b = _run_variant(pd, cfg, phi, mu, 120, True, blocks=(2, 2, 2), **kw)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_c2_full_100_steps(pv1):
+    # BASELINE config 2 at full size against the whole oracle trajectory
+    cfg, (phi, mu) = _state("c2", 128, 128, 128)
+    gphi, gmu, _ = _gpu_run(pv1, cfg, phi, mu, 100)
+    ophi, omu, _ = O.run(_oracle_params(pv1, cfg), phi, mu, 100)
+    assert O.rel_maxnorm(gphi, ophi) <= TOL100
+    assert O.rel_maxnorm(gmu, omu) <= TOL100
+
+
+@pytest.mark.parametrize("name,shape,steps", [("c2", (128, 128, 128), 1000), ("c4", (512, 512, 512), 500),
+                                              ("c3", (256, 256, 1024), 2000), ("c5", (1024, 1024, 256), 200)])
+def test_full_size_one_step_map_at_run_end(pv1, name, shape, steps):
+    # each config's full size and step count (BASELINE.json), in the bench's
+    # launch configuration: the GPU's last step from its own step-(n-1) state,
+    # against the oracle's one-step map on sampled cells (front band + random)
+    pf = _pf()
+    nx, ny, nz = shape
+    cfg, (phi, mu) = _state(name, nx, ny, nz)
+    prm = pf.make_params(pv1, cfg, nx=nx, ny=ny)
+    with pf.Context(nx, ny, nz, prm) as ctx:
+        ctx.write(phi, mu)
+        ctx.step(steps - 1)
+        inf = ctx.info()
+        sphi, smu = ctx.read()
+        ctx.step(1)
+        gphi, gmu = ctx.read()
+    assert np.abs(sphi - phi).max() > 1e-3        # the state evolved
+    cells = _sample_cells(nx, ny, nz, 3000)
+    lh = int(cfg["init"]["layer_height"])
+    rng = np.random.default_rng(2)
+    band = rng.integers(0, nx * ny, 3000) + (lh - 3 + rng.integers(0, 6, 3000)) * nx * ny
+    cells = np.concatenate([cells, band]).astype(np.int64)
+    po, mo = O.step_cells(_oracle_params(pv1, cfg), sphi, smu, cells, n=int(inf.step), zorig=int(inf.z_origin))
+    assert O.rel_maxnorm(gphi.reshape(4, -1)[:, cells], po) <= TOL1
+    assert O.rel_maxnorm(gmu.reshape(2, -1)[:, cells], mo) <= TOL1
