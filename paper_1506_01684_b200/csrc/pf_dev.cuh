@@ -23,17 +23,20 @@ constexpr int LIQ = 3;
 // pair index p of (a<b): (0,1)=0 (0,2)=1 (0,3)=2 (1,2)=3 (1,3)=4 (2,3)=5
 __host__ __device__ constexpr int pair_a(int p) { return p < 3 ? 0 : (p < 5 ? 1 : 2); }
 __host__ __device__ constexpr int pair_b(int p) { return p < 3 ? p + 1 : (p < 5 ? p - 1 : 3); }
+// pair index of {a, b}, a != b
+__host__ __device__ constexpr int pair_of(int a, int b) {
+  return a < b ? (a == 0 ? b - 1 : a + b) : (b == 0 ? a - 1 : a + b);
+}
 
 // Per-step constants (kernel argument, lives in the constant bank).
 struct KParams {
   double dt, inv_dt, inv_dx, inv_2dx, half_inv_dt;
   double dt_taueps[NPH];   // dt / (tau_a eps)
   double g2[6];            // 2 gamma_ab per pair
-  double gf4[6];           // 2 gamma_ab / (4 dx): isotropic face flux constant
-  double g2m[NPH][NPH];    // 2 gamma_ab as a matrix (0 on the diagonal)
-  double g2mc[NPH][NPH];   // 2 gamma_ab / (2 dx)^2: isotropic Gram of raw centre differences
+  double g2c[6];           // 2 gamma_ab / (2 dx)^2 per pair: isotropic Gram of raw centre differences
+  double gf2[6];           // gamma_ab / dx per pair: isotropic face flux on the lo/hi determinant
+  double omp[6];           // 16/pi^2 gamma_ab per pair
   double delta[6];         // cubic anisotropy per pair
-  double om[NPH][NPH];     // 16/pi^2 gamma_ab (0 on the diagonal)
   double g3[NPH];          // triple coefficient of the triple excluding x
   double pi_eps_4;         // pi eps / 4
   double Gv;               // G v = -dT/dt
@@ -123,14 +126,16 @@ __device__ __forceinline__ void phi_face(const KParams &kp, const double plo[NPH
   if (!kp.aniso) {
     // isotropic: with s = lo + hi = 2 phibar and t = hi - lo = dx grad_d phi,
     // j_a = -sum_b 2 gamma_ab (phibar_a grad_b - phibar_b grad_a) phibar_b
-    //     = -sum_b [2 gamma_ab / (4 dx)] (s_a t_b - s_b t_a) s_b   (gf4 = 2 gamma / 4 dx)
-    double s[NPH], t[NPH];
+    //     = -sum_b [2 gamma_ab / (4 dx)] (s_a t_b - s_b t_a) s_b,
+    // and s_a t_b - s_b t_a = 2 (lo_a hi_b - hi_a lo_b): a 2x2 determinant of
+    // the two cells (gf2 = gamma / dx), no cancellation in t
+    double s[NPH];
 #pragma unroll
-    for (int a = 0; a < NPH; ++a) { s[a] = RN_ADD(plo[a], phi_[a]); t[a] = RN_SUB(phi_[a], plo[a]); }
+    for (int a = 0; a < NPH; ++a) s[a] = RN_ADD(plo[a], phi_[a]);
 #pragma unroll
     for (int p = 0; p < 6; ++p) {
       const int a = pair_a(p), b = pair_b(p);
-      const double G = RN_MUL(kp.gf4[p], RN_FMA(s[a], t[b], -RN_MUL(s[b], t[a])));
+      const double G = RN_MUL(kp.gf2[p], RN_FMA(plo[a], phi_[b], -RN_MUL(phi_[a], plo[b])));
       jf[a] = RN_FMA(-G, s[b], jf[a]);
       jf[b] = RN_FMA(G, s[a], jf[b]);
     }
@@ -220,7 +225,7 @@ __device__ __forceinline__ void phi_cell_rhs0(const KParams &kp, const double *_
 #pragma unroll
     for (int p = 0; p < 6; ++p) {
       const int a = pair_a(p), b = pair_b(p);
-      Go[p] = kp.g2mc[a][b] * (gc[a][0] * gc[b][0] + gc[a][1] * gc[b][1] + gc[a][2] * gc[b][2]);
+      Go[p] = kp.g2c[p] * (gc[a][0] * gc[b][0] + gc[a][1] * gc[b][1] + gc[a][2] * gc[b][2]);
     }
 #pragma unroll
     for (int a = 0; a < NPH; ++a) {
@@ -228,8 +233,8 @@ __device__ __forceinline__ void phi_cell_rhs0(const KParams &kp, const double *_
 #pragma unroll
       for (int b = 0; b < NPH; ++b) {
         if (b == a) continue;
-        const int p = a < b ? (a == 0 ? b - 1 : a + b) : (b == 0 ? a - 1 : a + b);   // pair index of {a,b}
-        wd += kp.g2mc[a][b] * Gd[b];
+        const int p = pair_of(a, b);
+        wd += kp.g2c[p] * Gd[b];
         wo += ph[b] * Go[p];
       }
       dad[a] = ph[a] * wd - wo;
@@ -275,14 +280,14 @@ __device__ __forceinline__ void phi_cell_rhs0(const KParams &kp, const double *_
     // O4.7 multi-obstacle derivative
     double om = 0.0;
 #pragma unroll
-    for (int b = 0; b < NPH; ++b) if (b != a) om += kp.om[a][b] * ph[b];
+    for (int b = 0; b < NPH; ++b) if (b != a) om += kp.omp[pair_of(a, b)] * ph[b];
 #pragma unroll
     for (int x = 0; x < NPH; ++x) {
       if (x == a) continue;
       int b = -1, e = -1;
 #pragma unroll
       for (int y = 0; y < NPH; ++y) if (y != a && y != x) { if (b < 0) b = y; else e = y; }
-      om += kp.g3[x] * pp[b == 0 ? e - 1 : b + e];   // pair index of {b < e}
+      om += kp.g3[x] * pp[pair_of(b, e)];
     }
     // O4.8 driving force
     const double dpsi = (ph[a] * rS2) * (ps[a] - pbar);
@@ -295,30 +300,25 @@ __device__ __forceinline__ void phi_cell_finish(const KParams &kp, const double 
                                                 const double dsum[NPH], double out[NPH]) {
   // O4.9 with the O4.6 divergence of the face fluxes (eps T / dx folded)
   const double epsTdx = tab[T_EPSTDX];
-  double rhs[NPH], sum = 0.0;
+  double rhs[NPH];
 #pragma unroll
-  for (int a = 0; a < NPH; ++a) {
-    rhs[a] = r0[a] - epsTdx * dsum[a];
-    sum += rhs[a];
-  }
-  const double mean = 0.25 * sum;
+  for (int a = 0; a < NPH; ++a) rhs[a] = r0[a] - epsTdx * dsum[a];
+  const double mean = 0.25 * ((rhs[0] + rhs[1]) + (rhs[2] + rhs[3]));
   double x[NPH];
 #pragma unroll
   for (int a = 0; a < NPH; ++a) x[a] = ph[a] - kp.dt_taueps[a] * (rhs[a] - mean);   // O4.10 (minus sign, R1)
 
   // O4.11 Euclidean projection onto the simplex: sort descending (network),
-  // theta = (sum of the rho largest - 1)/rho with rho the largest j such that
-  // u_j > (sum_{r<=j} u_r - 1)/j.
+  // theta = t_rho = (sum of the rho largest - 1)/rho with rho the largest j
+  // such that u_j > t_j.  Since t_{j+1} - t_j = (u_{j+1} - t_j)/(j+1), t_j
+  // rises while j < rho and falls after, so theta = max_j t_j: a max tree
+  // instead of a chain of dependent selects (same value up to rounding ties).
   double u0 = x[0], u1 = x[1], u2 = x[2], u3 = x[3], t;
 #define PF_CSWAP(p, q) if (p < q) { t = p; p = q; q = t; }
   PF_CSWAP(u0, u1) PF_CSWAP(u2, u3) PF_CSWAP(u0, u2) PF_CSWAP(u1, u3) PF_CSWAP(u1, u2)
 #undef PF_CSWAP
   const double c1 = u0 - 1.0, c2 = c1 + u1, c3 = c2 + u2, c4 = c3 + u3;
-  const double t1 = c1, t2 = 0.5 * c2, t3 = c3 * (1.0 / 3.0), t4 = 0.25 * c4;
-  double theta = t1;
-  if (u1 - t2 > 0.0) theta = t2;
-  if (u2 - t3 > 0.0) theta = t3;
-  if (u3 - t4 > 0.0) theta = t4;
+  const double theta = fmax(fmax(c1, 0.5 * c2), fmax(c3 * (1.0 / 3.0), 0.25 * c4));
 #pragma unroll
   for (int a = 0; a < NPH; ++a) out[a] = fmax(x[a] - theta, 0.0);
 }

@@ -822,13 +822,12 @@ pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
   for (int a = 0; a < 4; ++a) {
     kp.dt_taueps[a] = p->dt / (p->tau[a] * p->eps);
     kp.g3[a] = p->gamma3[a];
-    for (int b = 0; b < 4; ++b) kp.om[a][b] = a == b ? 0.0 : 16.0 / (M_PI * M_PI) * p->gamma[a][b];
-    for (int b = 0; b < 4; ++b) kp.g2m[a][b] = a == b ? 0.0 : 2.0 * p->gamma[a][b];
-    for (int b = 0; b < 4; ++b) kp.g2mc[a][b] = kp.g2m[a][b] * kp.inv_2dx * kp.inv_2dx;
   }
   for (int q = 0; q < 6; ++q) {
     kp.g2[q] = 2.0 * p->gamma[pair_a(q)][pair_b(q)];
-    kp.gf4[q] = kp.g2[q] * 0.25 / p->dx;
+    kp.gf2[q] = kp.g2[q] * 0.5 / p->dx;
+    kp.g2c[q] = kp.g2[q] * kp.inv_2dx * kp.inv_2dx;
+    kp.omp[q] = 16.0 / (M_PI * M_PI) * p->gamma[pair_a(q)][pair_b(q)];
     kp.delta[q] = p->aniso ? p->delta[pair_a(q)][pair_b(q)] : 0.0;
   }
   kp.pi_eps_4 = M_PI * p->eps / 4.0;
