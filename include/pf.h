@@ -141,8 +141,9 @@ pf_status pf_nccl_unique_id(uint8_t out[128]);
 /* Host-only query of the halo message plan (no GPU needed): for rank g->rank,
  * the number of doubles it sends to (send_counts[r]) and receives from
  * (recv_counts[r]) every rank r in one ghost-layer exchange of `field`
- * (0 = phi, 4 components; 1 = mu, 2 components).  Faces and the 12 edges of
- * every block; periodic x/y, zero-flux z.  Both arrays hold
+ * (0 = phi, 4 components; 1 = mu, 2 components).  Faces, the 12 edges (the
+ * D3C19 stencil) and the 8 corner cells (marching cubes,
+ * PAPER.md:249-250) of every block; periodic x/y, zero-flux z.  Both arrays hold
  * g->nranks entries (caller-owned).  Errors: PF_ERR_ARG, PF_ERR_CONFIG. */
 pf_status pf_halo_plan(const pf_grid *g, int32_t field, int64_t *send_counts, int64_t *recv_counts);
 

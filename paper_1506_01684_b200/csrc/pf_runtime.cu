@@ -1,8 +1,9 @@
 // pf_runtime.cu — host runtime behind the C ABI of include/pf.h.
 //
 // Owns: the block decomposition ("equal-size blocks", one per
-// GPU rank or several per GPU), the fields (FP64, SoA, padded rows, one ghost
-// layer incl. the 12 edges the D3C19 stencil needs), the
+// GPU rank or several per GPU), the fields (FP64, SoA, padded rows, one full
+// ghost layer: the 12 edges the D3C19 stencil needs, and the 8
+// corners the marching cubes read), the
 // per-plane table, the halo plans (local device copies + NCCL grouped
 // send/recv), the moving window and the
 // NaN watchdog ("no silent NaN propagation").
@@ -154,14 +155,15 @@ inline int64_t cell_off(const Block &b, int64_t i, int64_t j, int64_t k) {
 int block_id(const pf_ctx *c, int bx, int by, int bz) { return bx + c->g.px * (by + c->g.py * bz); }
 int owner_rank(const pf_ctx *c, int bid) { return c->g.nranks == 1 ? 0 : bid; }
 
-// the 18 ghost directions: faces and edges (corners unused by D3C19)
+// the 26 ghost directions: faces and edges (the D3C19 stencil) and corners (one
+// cell each; the marching cubes at a block's far corner read them)
 std::vector<std::array<int, 3>> ghost_dirs() {
   std::vector<std::array<int, 3>> v;
   for (int dz = -1; dz <= 1; ++dz)
     for (int dy = -1; dy <= 1; ++dy)
       for (int dx = -1; dx <= 1; ++dx) {
         const int m = std::abs(dx) + std::abs(dy) + std::abs(dz);
-        if (m == 1 || m == 2) v.push_back({dx, dy, dz});
+        if (m >= 1) v.push_back({dx, dy, dz});
       }
   return v;
 }

@@ -67,8 +67,9 @@ def test_gloo_plan_symmetry_and_bootstrap(world):
                 for b in range(world):
                     assert allt[a][0][b] == allt[b][1][a]   # a->b send == b<-a recv
             ncomp = 4 if field == 0 else 2
-            # 2x1x1 of 64^3 blocks, periodic x: both x faces and the 8 x-edges come from the peer
-            assert allt[0][1][1] == ncomp * (2 * 64 * 64 + 8 * 64)
+            # 2x1x1 of 64^3 blocks, periodic x: both x faces, the 8 x-edges and the
+            # 8 corners come from the peer
+            assert allt[0][1][1] == ncomp * (2 * 64 * 64 + 8 * 64 + 8)
 
 
 def test_plan_8_ranks_in_process():
@@ -91,7 +92,8 @@ def test_plan_8_ranks_in_process():
             # edges: 4 xy-edges (peers), 4 xz/yz edges toward the z peer, the 4
             # toward the wall come from the x/y peers (clamped) -> all remote
             edges = 4 * n + 8 * n
-            assert sum(plans[r][1]) == ncomp * (faces + edges), (r, bx, by, bz)
+            corners = 8          # every corner has dx != 0: an x peer
+            assert sum(plans[r][1]) == ncomp * (faces + edges + corners), (r, bx, by, bz)
 
 
 def test_plan_single_rank_has_no_messages():
