@@ -304,6 +304,9 @@ def run_gpu(args):
                                         "measured DFMA loop 34.2 TFLOP/s",
                          "sweeps": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv)
                                         for kk, vv in s.items()} for k, s in sweeps.items()},
+                         "note": "flop = algorithmic FLOP/LUP counted from the oracle with every term evaluated "
+                                 "(PAPER.md:508-509); the mu-sweep's exact-zero anti-trapping guards skip most "
+                                 "of its FP64 work on bulk planes, so mu is judged by frac_hbm (96 B/LUP)",
                          "hbm_peak_gbs": hbm},
             "cpu_baseline": {"value": round(cpu_v, 3) if cpu_v else None, "unit": "MLUP/s", "cores": cores,
                              "kind": "oracle", "sample": sample},
