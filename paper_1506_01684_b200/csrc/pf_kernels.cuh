@@ -9,9 +9,24 @@
 namespace pf {
 
 constexpr int XO = 4;  // column of interior i = 0 within a padded row (i = -1 at 3)
-// CTA tiles of the z-marching sweeps (pf_tile.cuh): 32 x 4 for the phi-sweep
-// (4 CTAs / SM), 32 x 8 for the mu-sweep (2 CTAs / SM) — measured best.
-constexpr int TILE_X = 32, PHI_TILE_Y = 4, MU_TILE_Y = 8;
+// CTA tiles of the z-marching sweeps (pf_tile.cuh), measured best (tools/ab_*):
+// 16 x 8 for the phi-sweep (128 threads, each warp two rows; 4 CTAs / SM; the
+// 24 far faces of a plane fit one warp — 32 x 4: 4.16 ms, 16 x 8: 4.09 ms,
+// 16 x 16: 4.21, 8 x 16: 5.4 at 512^3), 32 x 8 for the mu-sweep (2 CTAs / SM;
+// 16 x 16: +4 %).  -DPF_PHI_TX/TY, -DPF_MU_TX/TY override for experiments.
+#ifndef PF_PHI_TX
+#define PF_PHI_TX 16
+#endif
+#ifndef PF_PHI_TY
+#define PF_PHI_TY 8
+#endif
+#ifndef PF_MU_TX
+#define PF_MU_TX 32
+#endif
+#ifndef PF_MU_TY
+#define PF_MU_TY 8
+#endif
+constexpr int PHI_TILE_X = PF_PHI_TX, PHI_TILE_Y = PF_PHI_TY, MU_TILE_X = PF_MU_TX, MU_TILE_Y = PF_MU_TY;
 
 // TMA descriptors of one block's fields in one time level (encoded on the host
 // over the whole padded allocation: dims {pitch, ny+2, planes}, x fastest).

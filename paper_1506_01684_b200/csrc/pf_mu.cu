@@ -21,6 +21,7 @@
 // come from registers.  All arithmetic is the pinned code of pf_dev.cuh, so
 // results do not depend on tile or block boundaries.
 #include "pf_kernels.cuh"
+#define PF_TILE_X MU_TILE_X
 #define PF_TILE_Y MU_TILE_Y
 #include "pf_tile.cuh"
 

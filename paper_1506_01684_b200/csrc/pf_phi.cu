@@ -13,6 +13,7 @@
 // gradient routines are the pinned ones of pf_dev.cuh: a face evaluated at a
 // tile / chunk / block edge has the same bits as mid-tile.
 #include "pf_kernels.cuh"
+#define PF_TILE_X PHI_TILE_X
 #define PF_TILE_Y PHI_TILE_Y
 #include "pf_tile.cuh"
 

@@ -246,15 +246,15 @@ pf_status encode_map(pf_ctx *c, CUtensorMap *m, double *base, const Block &b, in
 
 pf_status encode_maps(pf_ctx *c, Block &b) {
   for (int cp = 0; cp < 2; ++cp) {
-    // tile boxes start one column left of the ring (16-byte aligned x): TILE_X + 4 wide;
+    // tile boxes start one column left of the ring (16-byte aligned x): tile width + 4;
     // phi-sweep tiles are PHI_TILE_Y high, mu-sweep tiles MU_TILE_Y
     for (int a = 0; a < NPH; ++a) {
-      CKS(encode_map(c, &b.tphi[cp][a], b.phi[cp][a], b, TILE_X + 4, PHI_TILE_Y + 2));
-      CKS(encode_map(c, &b.tphim[cp][a], b.phi[cp][a], b, TILE_X + 4, MU_TILE_Y + 2));
+      CKS(encode_map(c, &b.tphi[cp][a], b.phi[cp][a], b, PHI_TILE_X + 4, PHI_TILE_Y + 2));
+      CKS(encode_map(c, &b.tphim[cp][a], b.phi[cp][a], b, MU_TILE_X + 4, MU_TILE_Y + 2));
     }
     for (int q = 0; q < NMU; ++q) {
-      CKS(encode_map(c, &b.tmu[cp][q], b.mu[cp][q], b, TILE_X + 4, MU_TILE_Y + 2));
-      CKS(encode_map(c, &b.tmui[cp][q], b.mu[cp][q], b, TILE_X, PHI_TILE_Y));
+      CKS(encode_map(c, &b.tmu[cp][q], b.mu[cp][q], b, MU_TILE_X + 4, MU_TILE_Y + 2));
+      CKS(encode_map(c, &b.tmui[cp][q], b.mu[cp][q], b, PHI_TILE_X, PHI_TILE_Y));
     }
   }
   return PF_OK;

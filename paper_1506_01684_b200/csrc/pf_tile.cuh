@@ -13,10 +13,10 @@
 
 namespace pf {
 
-#ifndef PF_TILE_Y
-#error "define PF_TILE_Y (the CTA tile height) before including pf_tile.cuh"
+#if !defined(PF_TILE_X) || !defined(PF_TILE_Y)
+#error "define PF_TILE_X / PF_TILE_Y (the CTA tile) before including pf_tile.cuh"
 #endif
-constexpr int TX = TILE_X, TY = PF_TILE_Y, RX = TX + 2, RY = TY + 2;
+constexpr int TX = PF_TILE_X, TY = PF_TILE_Y, RX = TX + 2, RY = TY + 2;
 constexpr int NTHR = TX * TY;
 constexpr int NRING = 2 * RX + 2 * TY;  // 84 ring cells incl. the 4 in-plane corners
 constexpr int NSLOT = 4;                // plane slots: k-1, k, k+1 in use, k+2 in flight
