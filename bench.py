@@ -94,6 +94,16 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def load_cfg(name):
     return json.load(open(os.path.join(ROOT, "configs", f"{name}.json")))
 
@@ -309,7 +319,11 @@ def run_gpu(args):
                                  "of its FP64 work on bulk planes, so mu is judged by frac_hbm (96 B/LUP)",
                          "hbm_peak_gbs": hbm},
             "cpu_baseline": {"value": round(cpu_v, 3) if cpu_v else None, "unit": "MLUP/s", "cores": cores,
+                             "per_core": round(cpu_v / cores, 3) if cpu_v else None, "cpu": cpu_model(),
                              "kind": "oracle", "sample": sample},
+            "paper_context": {"mlups_per_core": 4.2, "what": "mu-kernel only (no phi), one SuperMUC Sandy Bridge "
+                              "core, SIMD-optimised, Ag-Al-Cu parameters (PAPER.md:526); the paper prints no GPU "
+                              "or full-step number", "unit": "MLUP/s/core"},
             "e2e": {"value": round(e2e, 2) if e2e else None, "unit": "MLUP/s",
                     "h2d_bytes_per_step": state_bytes if e2e else 0,
                     "d2h_bytes_per_step": state_bytes if e2e else 0, "steps": e2e_steps,
