@@ -451,34 +451,43 @@ __device__ __forceinline__ void mu_face(const KParams &kp, const MuQ &lo, const 
 __device__ __forceinline__ void mu_cell_update(const KParams &kp, const double *__restrict__ tab,
                                                const double po[NPH], const double pn[NPH], const double mu[NMU],
                                                const double divf[NMU], double out[NMU]) {
-  const double So = po[0] * po[0] + po[1] * po[1] + po[2] * po[2] + po[3] * po[3];
-  const double Sn = pn[0] * pn[0] + pn[1] * pn[1] + pn[2] * pn[2] + pn[3] * pn[3];
-  // one reciprocal for both 1/S (S in [1/4, 1] on the simplex)
-  const double rS = 1.0 / (So * Sn), rSo = Sn * rS, rSn = So * rS;
-  double hn[NPH], dh[NPH];
+  // With p = (phi^n)^2, q = (phi^{n+1})^2 (componentwise), S = sum: h^n = p/So,
+  // h^{n+1} = q/Sn, chi_c = X_c/Sn with X_c = sum_a q_a/(2A_a) (O5.3), so
+  //   s_c    = sum_a e_ca (q_a/Sn - p_a/So),  e_ca = mu_c/(2A_a) + chat_a  (O5.4)
+  //   dcdT_c = (1/Sn) sum_a q_a (m_a - mu_c kappa_a)                      (O5.5)
+  //   mu_c^{n+1} = mu_c + (dt Sn / X_c) [dcdT_c G v - s_c/dt + div_c]     (O5.9)
+  // and one reciprocal R = 1/(So Sn X_0 X_1) serves 1/So, 1/Sn, 1/X_0, 1/X_1.
+  double p[NPH], q[NPH];
 #pragma unroll
-  for (int a = 0; a < NPH; ++a) {
-    hn[a] = pn[a] * pn[a] * rSn;
-    dh[a] = hn[a] - po[a] * po[a] * rSo;
-  }
-  double chi[NMU] = {0.0, 0.0}, s[NMU] = {0.0, 0.0}, dcdT[NMU] = {0.0, 0.0}, rest[NMU];
+  for (int a = 0; a < NPH; ++a) { p[a] = po[a] * po[a]; q[a] = pn[a] * pn[a]; }
+  const double So = (p[0] + p[1]) + (p[2] + p[3]), Sn = (q[0] + q[1]) + (q[2] + q[3]);
+  double X[NMU] = {0.0, 0.0}, A[NMU] = {0.0, 0.0}, B[NMU] = {0.0, 0.0}, D[NMU] = {0.0, 0.0};
 #pragma unroll
   for (int a = 0; a < NPH; ++a) {
     const double2 i2a = tab2(tab, T_INV2A, a), ch = tab2(tab, T_CHAT, a);
     const double2 mc = tab2(tab, T_MCHAT, a), ka = tab2(tab, T_KAPPA, a);
-    chi[0] += hn[a] * i2a.x;                                  // O5.3
-    chi[1] += hn[a] * i2a.y;
-    s[0] += (mu[0] * i2a.x + ch.x) * dh[a];                   // O5.4 (sign below)
-    s[1] += (mu[1] * i2a.y + ch.y) * dh[a];
-    dcdT[0] += hn[a] * (mc.x - mu[0] * ka.x);                 // O5.5
-    dcdT[1] += hn[a] * (mc.y - mu[1] * ka.y);
+    const double e0 = mu[0] * i2a.x + ch.x, e1 = mu[1] * i2a.y + ch.y;
+    X[0] += q[a] * i2a.x;
+    X[1] += q[a] * i2a.y;
+    A[0] += e0 * q[a];
+    A[1] += e1 * q[a];
+    B[0] += e0 * p[a];
+    B[1] += e1 * p[a];
+    D[0] += q[a] * (mc.x - mu[0] * ka.x);
+    D[1] += q[a] * (mc.y - mu[1] * ka.y);
   }
+  const double P = So * Sn, Q = X[0] * X[1];
+  const double R = 1.0 / (P * Q);
+  const double QR = Q * R, PR = P * R;
+  const double rSn = So * QR, rSo = Sn * QR;           // 1/Sn, 1/So
+  const double dtSn = kp.dt * Sn;
+  const double f[NMU] = {dtSn * (PR * X[1]), dtSn * (PR * X[0])};   // dt Sn / X_c
 #pragma unroll
-  for (int c = 0; c < NMU; ++c) rest[c] = dcdT[c] * kp.Gv - s[c] * kp.inv_dt + divf[c] * kp.inv_dx;
-  // mu^{n+1} = mu + dt/chi [ -s/dt + dcdT G v + div ]; one reciprocal for both chi
-  const double rc = kp.dt / (chi[0] * chi[1]);
-  out[0] = mu[0] + (chi[1] * rc) * rest[0];
-  out[1] = mu[1] + (chi[0] * rc) * rest[1];
+  for (int c = 0; c < NMU; ++c) {
+    const double sc = A[c] * rSn - B[c] * rSo;
+    const double rest = (D[c] * rSn) * kp.Gv - sc * kp.inv_dt + divf[c] * kp.inv_dx;
+    out[c] = mu[c] + f[c] * rest;
+  }
 }
 
 // Algorithm 2's second half: add the anti-trapping
