@@ -123,12 +123,11 @@ def workload(name: str, world: int):
     return cfg, (NX, NY, NZ), blocks, NX * NY * NZ // world, scaling
 
 
-def flops_per_lup(cfg):
-    from oracle import oracle as O
-    from inputs import gen
-    pd = gen.load_params("v1")
-    return O.count_flops(O.make_params(pd, layer_height=cfg["init"]["layer_height"], aniso=cfg.get("aniso", False),
-                                       delta_sl=cfg.get("delta_sl")))
+def flops_per_lup(name):
+    """Algorithmic FLOP/LUP of the config's sweeps, as counted from the oracle's
+    source by tools/count_flops.py (committed in profiles/flop_counts.json)."""
+    d = json.load(open(os.path.join(ROOT, "profiles", "flop_counts.json")))
+    return d["configs"][name]
 
 
 def cpu_oracle_sample(name: str, steps: int, nz_slab: int = 16):
@@ -269,7 +268,7 @@ def run_gpu(args):
         del hphi, hmu
 
     if rank == 0:
-        fl = flops_per_lup(cfg)
+        fl = flops_per_lup(args.config)
         peaks = {}
         try:
             peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))

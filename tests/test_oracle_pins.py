@@ -683,3 +683,19 @@ def test_p16_cube_cases_exhaustive():
         for (a, b), n in sides.items():
             on_face = any(set(MC.EDGES[a][:2]) | set(MC.EDGES[b][:2]) <= set(f) for f in MC.FACES)
             assert n == 1 and (sides.get((b, a), 0) == (0 if on_face else 1)), (case, a, b)
+
+
+def test_committed_flop_counts_match_oracle():
+    # bench.py's roofline reads profiles/flop_counts.json (written by
+    # tools/count_flops.py); it must be the oracle's own count
+    import json
+    import os
+    from inputs import gen
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    d = json.load(open(os.path.join(root, "profiles", "flop_counts.json")))["configs"]
+    pd = gen.load_params("v1")
+    for name, fl in d.items():
+        cfg = gen.load_config(name)
+        ref = O.count_flops(O.make_params(pd, layer_height=cfg["init"]["layer_height"], aniso=cfg.get("aniso", False),
+                                          delta_sl=cfg.get("delta_sl")))
+        assert {k: int(v) for k, v in ref.items()} == fl, name
