@@ -327,3 +327,48 @@ def test_full_size_one_step_map_at_run_end(pv1, name, shape, steps):
     po, mo = O.step_cells(_oracle_params(pv1, cfg), sphi, smu, cells, n=int(inf.step), zorig=int(inf.z_origin))
     assert O.rel_maxnorm(gphi.reshape(4, -1)[:, cells], po) <= TOL1
     assert O.rel_maxnorm(gmu.reshape(2, -1)[:, cells], mo) <= TOL1
+
+
+def _crafted(kind, nx, ny, nz, seed):
+    """Admissible crafted states (SURVEY.md §4 layer 3): every phase vector on
+    the Gibbs simplex; mu in [-0.3, 0.3]."""
+    rng = np.random.default_rng(seed)
+    mu = rng.uniform(-0.3, 0.3, (2, nz, ny, nx))
+    if kind == "random":          # every face a multi-phase interface: all anti-trapping guards open
+        phi = rng.random((4, nz, ny, nx)) ** 3
+        phi[rng.random((4, nz, ny, nx)) < 0.2] = 0.0
+        phi[3] += 1e-3                # no empty cell
+    elif kind == "triple":        # three phases meeting along z-lines + liquid above
+        x, y = np.meshgrid(np.arange(nx) + 0.5, np.arange(ny) + 0.5)
+        ang = np.arctan2(y - ny / 2, x - nx / 2)
+        phi = np.zeros((4, nz, ny, nx))
+        for a in range(3):
+            w = np.clip(1.0 - np.abs(((ang - 2 * np.pi * a / 3 + np.pi) % (2 * np.pi)) - np.pi) / (np.pi / 1.5), 0, 1)
+            phi[a] = w[None]
+        z = np.arange(nz)[:, None, None] + 0.5
+        s = np.clip(0.5 + (nz / 2 - z) / 4, 0, 1)
+        phi[:3] *= s
+        phi[3] = 1 - s + 1e-3
+    else:                         # binary 1D alpha|liquid front along x
+        x = np.arange(nx) + 0.5
+        r = np.clip(0.5 + (nx / 2 - x) / 4, 0, 1)
+        phi = np.zeros((4, nz, ny, nx))
+        phi[0] = r[None, None, :]
+        phi[3] = 1 - r[None, None, :]
+    phi /= phi.sum(axis=0, keepdims=True)
+    return phi, mu
+
+
+@pytest.mark.parametrize("kind", ["random", "triple", "binary"])
+@pytest.mark.parametrize("aniso", [False, True])
+def test_crafted_states_one_step(pv1, kind, aniso):
+    nx, ny, nz = 21, 18, 14
+    cfg = gen.load_config("c5" if aniso else "c2")
+    phi, mu = _crafted(kind, nx, ny, nz, seed=11)
+    gphi, gmu, _ = _gpu_run(pv1, cfg, phi, mu, 1, window=False, layer_height=7, blocks=(1, 1, 1))
+    ophi, omu = O.step(_oracle_params(pv1, cfg, layer_height=7), phi, mu)
+    assert O.rel_maxnorm(gphi, ophi) <= 1e-12
+    assert O.rel_maxnorm(gmu, omu) <= 1e-12
+    # the same state split over blocks: bitwise
+    bphi, bmu, _ = _gpu_run(pv1, cfg, phi, mu, 1, window=False, layer_height=7, blocks=(1, 2, 2))
+    assert np.array_equal(bphi, gphi) and np.array_equal(bmu, gmu)
