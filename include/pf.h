@@ -115,6 +115,10 @@ typedef struct {
                                    mu halo is not hidden;
                                  3: both (Algorithm 2).
                                  Results of 2/3 differ from 0/1 by rounding only. */
+  int32_t no_graph;           /* 0 (default): single-rank runs without per-sweep
+                                 timing replay each step as a CUDA graph (one
+                                 launch per step); 1: launch the kernels one by one.
+                                 Results are identical. */
 } pf_params;
 
 /* Run-time information about a context. */

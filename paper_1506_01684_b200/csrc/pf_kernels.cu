@@ -10,9 +10,11 @@ namespace pf {
 // a1: per-plane coefficient table.  One thread per
 // global window plane kg = -1..NZ; T = T0 + G((kg + zorig + 1/2) dx - v n dt).
 // ---------------------------------------------------------------------------
-__global__ void table_kernel(double *tab, int64_t nplanes, TabParams tp, int64_t step, int64_t zorig) {
+__global__ void table_kernel(double *tab, int64_t nplanes, TabParams tp, int64_t step, int64_t zorig,
+                             const int64_t *d_step) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= nplanes) return;
+  if (d_step) step = *d_step;   // graph replays: the time level lives on the device
   const int64_t kg = r - 1;
   const double z = ((double)(kg + zorig) + 0.5) * tp.dx;
   const double T = tp.T0 + tp.G * (z - tp.v * ((double)step * tp.dt));
@@ -42,9 +44,13 @@ __global__ void table_kernel(double *tab, int64_t nplanes, TabParams tp, int64_t
     }
 }
 
-void launch_table(cudaStream_t s, double *tab, int64_t nplanes, const TabParams &tp, int64_t step, int64_t zorig) {
-  table_kernel<<<(unsigned)((nplanes + 127) / 128), 128, 0, s>>>(tab, nplanes, tp, step, zorig);
+void launch_table(cudaStream_t s, double *tab, int64_t nplanes, const TabParams &tp, int64_t step, int64_t zorig,
+                  const int64_t *d_step) {
+  table_kernel<<<(unsigned)((nplanes + 127) / 128), 128, 0, s>>>(tab, nplanes, tp, step, zorig, d_step);
 }
+
+__global__ void step_inc_kernel(int64_t *d_step) { *d_step += 1; }
+void launch_step_inc(cudaStream_t s, int64_t *d_step) { step_inc_kernel<<<1, 1, 0, s>>>(d_step); }
 
 // ---------------------------------------------------------------------------
 // Naive phi-sweep: one thread per cell, every neighbour read from global

@@ -80,9 +80,14 @@ struct TabParams {
   double A0[NPH][NMU], A1[NPH][NMU], c0[NPH][NMU], m[NPH][NMU], L[NPH], D[NPH][NMU];
 };
 // table rows for global window planes kg = -1 .. nplanes-2 (row = kg + 1)
-void launch_table(cudaStream_t s, double *tab, int64_t nplanes, const TabParams &tp, int64_t step, int64_t zorig);
+// d_step != nullptr: the time level is read from device memory (CUDA graph replays)
+void launch_table(cudaStream_t s, double *tab, int64_t nplanes, const TabParams &tp, int64_t step, int64_t zorig,
+                  const int64_t *d_step = nullptr);
+void launch_step_inc(cudaStream_t s, int64_t *d_step);
 void launch_phi_naive(cudaStream_t s, const KParams &kp, const BlockView &b);
 void launch_mu_naive(cudaStream_t s, const KParams &kp, const BlockView &b);
+void prepare_phi_tiled();   // shared-memory opt-in of the tiled sweeps (once, outside captures)
+void prepare_mu_tiled();
 void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm);
 // mu-sweep modes: the whole update (Algorithm 1), or Algorithm 2's split
 // into the part without the anti-trapping current and the

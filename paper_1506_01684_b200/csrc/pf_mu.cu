@@ -377,15 +377,21 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
 #undef T
 }
 
+// Opt-in to > 48 KB of dynamic shared memory, once per process (pf_create;
+// not inside a stream capture).
+void prepare_mu_tiled() {
+  const int sm = (int)sizeof(MuSmem);
+  cudaFuncSetAttribute(mu_tiled_kernel<MU_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(mu_tiled_kernel<MU_LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(mu_tiled_kernel<MU_NEIGHBOR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+}
+
 template <int MODE>
 void launch_mu_mode(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm) {
   const int gx = (b.nx + TX - 1) / TX, gy = (b.ny + TY - 1) / TY;
   const int kz = chunk_z(b.nz, gx * gy);
   dim3 grd(gx, gy, (b.nz + kz - 1) / kz), blk(TX, TY);
-  const size_t sm = sizeof(MuSmem);
-  static bool attr = false;
-  if (!attr) { cudaFuncSetAttribute(mu_tiled_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr = true; }
-  mu_tiled_kernel<MODE><<<grd, blk, sm, s>>>(tm, kp, b, kz);
+  mu_tiled_kernel<MODE><<<grd, blk, sizeof(MuSmem), s>>>(tm, kp, b, kz);
 }
 
 void launch_mu_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm, int mode) {

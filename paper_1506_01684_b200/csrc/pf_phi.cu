@@ -246,19 +246,21 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
 #undef T
 }
 
+// Opt-in to > 48 KB of dynamic shared memory, once per process (pf_create;
+// not inside a stream capture).
+void prepare_phi_tiled() {
+  const int sm = (int)sizeof(PhiSmem);
+  cudaFuncSetAttribute(phi_tiled_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(phi_tiled_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+}
+
 void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm) {
   const int gx = (b.nx + TX - 1) / TX, gy = (b.ny + TY - 1) / TY;
   const int kz = chunk_z(b.nz, gx * gy);
   dim3 grd(gx, gy, (b.nz + kz - 1) / kz), blk(TX, TY);
   const size_t sm = sizeof(PhiSmem);
-  static bool attr[2] = {false, false};
-  if (kp.aniso) {
-    if (!attr[1]) { cudaFuncSetAttribute(phi_tiled_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr[1] = true; }
-    phi_tiled_kernel<true><<<grd, blk, sm, s>>>(tm, kp, b, kz);
-  } else {
-    if (!attr[0]) { cudaFuncSetAttribute(phi_tiled_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); attr[0] = true; }
-    phi_tiled_kernel<false><<<grd, blk, sm, s>>>(tm, kp, b, kz);
-  }
+  if (kp.aniso) phi_tiled_kernel<true><<<grd, blk, sm, s>>>(tm, kp, b, kz);
+  else phi_tiled_kernel<false><<<grd, blk, sm, s>>>(tm, kp, b, kz);
 }
 
 }  // namespace pf

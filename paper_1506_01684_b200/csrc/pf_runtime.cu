@@ -108,6 +108,11 @@ struct pf_ctx {
   size_t mesh_scratch_bytes = 0;
   void *mesh_out = nullptr;
   size_t mesh_out_bytes = 0;
+  // CUDA graphs of one step (single-rank, timing off): one per parity of the
+  // src copy, invalidated whenever the halo plans, the window or the origin change
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  int64_t graph_launches[2] = {0, 0};
+  int64_t *d_step = nullptr;       // device copy of the time level for the table kernel
 };
 
 namespace {
@@ -274,7 +279,13 @@ TmaMaps maps_of(const pf_ctx *c, const Block &b, int field) {
 }
 
 // Build the halo plans of both fields and both copies.
+void invalidate_graphs(pf_ctx *c) {
+  for (int q = 0; q < 2; ++q)
+    if (c->gexec[q]) { cudaGraphExecDestroy(c->gexec[q]); c->gexec[q] = nullptr; }
+}
+
 pf_status build_plans(pf_ctx *c) {
+  invalidate_graphs(c);   // captured launches hold the plans' device pointers
   const auto dirs = ghost_dirs();
   const int nb = c->nblocks_total;
   const Block &b0 = c->blocks[0];
@@ -900,7 +911,8 @@ pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
   }
   c->tab_planes = g->nz + 2;
   if (cudaMalloc(&c->d_tab, (size_t)c->tab_planes * TAB * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&c->d_red, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+      cudaMalloc(&c->d_red, 4 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMalloc(&c->d_step, sizeof(int64_t)) != cudaSuccess) {
     fail(c, PF_ERR_CUDA, "alloc table"); return bail(PF_ERR_CUDA);
   }
   if (g->nranks > 1) {
@@ -914,6 +926,8 @@ pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
     if (r != ncclSuccess) { fail(c, PF_ERR_COMM, "ncclCommSplit: %s", ncclGetErrorString(r)); return bail(PF_ERR_COMM); }
   }
   if (build_plans(c) != PF_OK) return bail(c->status);
+  prepare_phi_tiled();
+  prepare_mu_tiled();
   if (cudaDeviceSynchronize() != cudaSuccess) { fail(c, PF_ERR_CUDA, "setup sync"); return bail(PF_ERR_CUDA); }
   *out = c;
   return PF_OK;
@@ -1005,69 +1019,112 @@ pf_status pf_set_time(pf_ctx *c, int64_t step, int64_t z_origin) {
   c->step = step;
   c->zorig = z_origin;
   c->next_check = step;
+  invalidate_graphs(c);   // the origin is a captured table argument
+  return PF_OK;
+}
+
+// Enqueue one time step (Algorithm 1 / 2) on the
+// context's streams: table, phi-sweep, phi halo, mu-sweep(s), mu halo.
+// graph = true while capturing a CUDA graph: the table reads the time level
+// from d_step (incremented at the end) and the mu halo is exchanged in order
+// on the main stream (results identical to the hidden exchange).
+pf_status enqueue_step(pf_ctx *c, bool graph) {
+  {
+    TimedSpan ts(c, 3, 0);
+    launch_table(c->stream, c->d_tab, c->tab_planes, c->tp, c->step, c->zorig, graph ? c->d_step : nullptr);
+    c->launches++;
+  }
+  {  // phi-sweep (Algorithm 1 line 1)
+    TimedSpan ts(c, 0, (int)c->blocks.size());
+    for (const auto &b : c->blocks) {
+      const BlockView v = view(c, b, 0);
+      if (c->p.variant == 1) launch_phi_naive(c->stream, c->kp, v);
+      else launch_phi_tiled(c->stream, c->kp, v, maps_of(c, b, 0));
+      c->launches++;
+    }
+  }
+  CK(cudaGetLastError());
+  const int ov = c->p.overlap;
+  const bool hide_phi = (ov == 2 || ov == 3) && c->p.variant != 1, hide_mu = (ov == 0 || ov == 3) && !graph;
+  auto mu_sweep = [&](int mode) -> pf_status {
+    TimedSpan ts(c, 1, (int)c->blocks.size());
+    for (const auto &b : c->blocks) {
+      const BlockView v = view(c, b, 1);
+      if (c->p.variant == 1) launch_mu_naive(c->stream, c->kp, v);
+      else launch_mu_tiled(c->stream, c->kp, v, maps_of(c, b, 1), mode);
+      c->launches++;
+    }
+    CK(cudaGetLastError());
+    return PF_OK;
+  };
+  if (hide_phi) {
+    // Algorithm 2: phi_dst ghosts on the comm stream while
+    // mu-sweep-local (no anti-trapping current: phi_dst needed at the cell
+    // only) runs; mu-sweep-neighbor adds the current once the ghosts are in
+    CK(cudaEventRecord(c->ev_phi_done, c->stream));
+    CK(cudaStreamWaitEvent(c->cstream, c->ev_phi_done, 0));
+    CKS(exchange(c, 0, c->cur ^ 1, true));
+    CK(cudaEventRecord(c->ev_phi_halo, c->cstream));
+    CKS(join_mu(c));                  // mu_src ghosts (previous step's exchange)
+    CKS(mu_sweep(MU_LOCAL));
+    CK(cudaStreamWaitEvent(c->stream, c->ev_phi_halo, 0));
+    CKS(mu_sweep(MU_NEIGHBOR));
+  } else {
+    CKS(exchange(c, 0, c->cur ^ 1));  // lines 2-3: phi_dst ghosts + boundary
+    CKS(join_mu(c));                  // mu_src ghosts (previous step's overlapped exchange)
+    CKS(mu_sweep(MU_FULL));           // line 4
+  }
+  // lines 5-6: mu_dst ghosts + boundary.  The next phi-sweep reads mu at the
+  // cell centre only (D3C1), so this exchange can overlap
+  // it on the comm stream (the paper's mu communication hiding)
+  if (hide_mu) {
+    CK(cudaEventRecord(c->ev_mu_done, c->stream));
+    CK(cudaStreamWaitEvent(c->cstream, c->ev_mu_done, 0));
+    CKS(exchange(c, 1, c->cur ^ 1, true));
+    CK(cudaEventRecord(c->ev_mu_halo, c->cstream));
+    c->mu_pending = true;
+  } else {
+    CKS(exchange(c, 1, c->cur ^ 1));
+  }
+  if (graph) { launch_step_inc(c->stream, c->d_step); c->launches++; }
+  return PF_OK;
+}
+
+// Capture one step from src copy c->cur into c->gexec[c->cur].
+pf_status capture_step(pf_ctx *c) {
+  cudaGraph_t g = nullptr;
+  const int64_t l0 = c->launches;
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  const pf_status st = enqueue_step(c, true);
+  const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+  if (st != PF_OK) { if (g) cudaGraphDestroy(g); return st; }
+  CK(e);
+  const cudaError_t ei = cudaGraphInstantiate(&c->gexec[c->cur], g, 0);
+  cudaGraphDestroy(g);
+  CK(ei);
+  c->graph_launches[c->cur] = c->launches - l0;
+  c->launches = l0;
   return PF_OK;
 }
 
 pf_status pf_step(pf_ctx *c, int64_t n) {
   CKS(check_state(c, true));
   if (n < 0) return fail(c, PF_ERR_ARG, "negative step count");
+  // CUDA graphs for single-rank runs without per-sweep timing (the common
+  // case: one launch per step instead of five-plus; pf_params.no_graph = 1
+  // or pf_set_timing(1) runs the kernels eagerly — same results, bit for bit)
+  const bool use_graph = !c->timing && c->g.nranks == 1 && !c->p.no_graph && n > 0;
+  if (use_graph) {
+    CKS(join_mu(c));
+    CK(cudaMemcpyAsync(c->d_step, &c->step, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+  }
   for (int64_t s = 0; s < n; ++s) {
-    {
-      TimedSpan ts(c, 3, 0);
-      launch_table(c->stream, c->d_tab, c->tab_planes, c->tp, c->step, c->zorig);
-      c->launches++;
-    }
-    {  // phi-sweep (Algorithm 1 line 1)
-      TimedSpan ts(c, 0, (int)c->blocks.size());
-      for (const auto &b : c->blocks) {
-        const BlockView v = view(c, b, 0);
-        if (c->p.variant == 1) launch_phi_naive(c->stream, c->kp, v);
-        else launch_phi_tiled(c->stream, c->kp, v, maps_of(c, b, 0));
-        c->launches++;
-      }
-    }
-    CK(cudaGetLastError());
-    const int ov = c->p.overlap;
-    const bool hide_phi = (ov == 2 || ov == 3) && c->p.variant != 1, hide_mu = ov == 0 || ov == 3;
-    auto mu_sweep = [&](int mode) -> pf_status {
-      TimedSpan ts(c, 1, (int)c->blocks.size());
-      for (const auto &b : c->blocks) {
-        const BlockView v = view(c, b, 1);
-        if (c->p.variant == 1) launch_mu_naive(c->stream, c->kp, v);
-        else launch_mu_tiled(c->stream, c->kp, v, maps_of(c, b, 1), mode);
-        c->launches++;
-      }
-      CK(cudaGetLastError());
-      return PF_OK;
-    };
-    if (hide_phi) {
-      // Algorithm 2: phi_dst ghosts on the comm stream while
-      // mu-sweep-local (no anti-trapping current: phi_dst needed at the cell
-      // only) runs; mu-sweep-neighbor adds the current once the ghosts are in
-      CK(cudaEventRecord(c->ev_phi_done, c->stream));
-      CK(cudaStreamWaitEvent(c->cstream, c->ev_phi_done, 0));
-      CKS(exchange(c, 0, c->cur ^ 1, true));
-      CK(cudaEventRecord(c->ev_phi_halo, c->cstream));
-      CKS(join_mu(c));                  // mu_src ghosts (previous step's exchange)
-      CKS(mu_sweep(MU_LOCAL));
-      CK(cudaStreamWaitEvent(c->stream, c->ev_phi_halo, 0));
-      CKS(mu_sweep(MU_NEIGHBOR));
+    if (use_graph) {
+      if (!c->gexec[c->cur]) CKS(capture_step(c));
+      CK(cudaGraphLaunch(c->gexec[c->cur], c->stream));
+      c->launches += c->graph_launches[c->cur];
     } else {
-      CKS(exchange(c, 0, c->cur ^ 1));  // lines 2-3: phi_dst ghosts + boundary
-      CKS(join_mu(c));                  // mu_src ghosts (previous step's overlapped exchange)
-      CKS(mu_sweep(MU_FULL));           // line 4
-    }
-    // lines 5-6: mu_dst ghosts + boundary.  The next phi-sweep reads mu at the
-    // cell centre only (D3C1), so this exchange can overlap
-    // it on the comm stream (the paper's mu communication hiding)
-    if (hide_mu) {
-      CK(cudaEventRecord(c->ev_mu_done, c->stream));
-      CK(cudaStreamWaitEvent(c->cstream, c->ev_mu_done, 0));
-      CKS(exchange(c, 1, c->cur ^ 1, true));
-      CK(cudaEventRecord(c->ev_mu_halo, c->cstream));
-      c->mu_pending = true;
-    } else {
-      CKS(exchange(c, 1, c->cur ^ 1));
+      CKS(enqueue_step(c, false));
     }
     c->cur ^= 1;                        // line 7: swap
     c->step += 1;
@@ -1207,6 +1264,7 @@ pf_status pf_load(pf_ctx *c, const char *path) {
   CK(cudaStreamSynchronize(c->stream));
   c->step = (int64_t)step;
   c->zorig = (int64_t)zorig;
+  invalidate_graphs(c);
   c->next_check = c->step;
   c->last_front = -1;
   c->initialized = true;
@@ -1319,6 +1377,8 @@ void pf_destroy(pf_ctx *c) {
   }
   if (c->d_tab) cudaFree(c->d_tab);
   if (c->d_red) cudaFree(c->d_red);
+  if (c->d_step) cudaFree(c->d_step);
+  invalidate_graphs(c);
   if (c->d_stage) cudaFree(c->d_stage);
   if (c->d_mesh_f) cudaFree(c->d_mesh_f);
   if (c->mesh_scratch) cudaFree(c->mesh_scratch);
