@@ -1110,10 +1110,9 @@ pf_status capture_step(pf_ctx *c) {
 pf_status pf_step(pf_ctx *c, int64_t n) {
   CKS(check_state(c, true));
   if (n < 0) return fail(c, PF_ERR_ARG, "negative step count");
-  // CUDA graphs for single-rank runs without per-sweep timing (the common
-  // case: one launch per step instead of five-plus; pf_params.no_graph = 1
-  // or pf_set_timing(1) runs the kernels eagerly — same results, bit for bit)
-  const bool use_graph = !c->timing && c->g.nranks == 1 && !c->p.no_graph && n > 0;
+  // CUDA graphs (pf_params.graph = 1) for single-rank runs without per-sweep
+  // timing: one launch per step instead of five-plus — same results, bit for bit
+  const bool use_graph = !c->timing && c->g.nranks == 1 && c->p.graph && n > 0;
   if (use_graph) {
     CKS(join_mu(c));
     CK(cudaMemcpyAsync(c->d_step, &c->step, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));

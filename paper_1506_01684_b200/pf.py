@@ -55,7 +55,7 @@ class PfParams(ctypes.Structure):
                 ("window_phi_l", D), ("nan_check_every", I32), ("variant", I32), ("init_kind", I32),
                 ("init_n_seeds", I32), ("init_lam_wmin", I32), ("init_lam_wmax", I32),
                 ("init_planar_phase", I32), ("shortcuts", I32), ("init_layer_height", D),
-                ("init_iface_width", D), ("init_mu_noise", D), ("overlap", I32), ("no_graph", I32)]
+                ("init_iface_width", D), ("init_mu_noise", D), ("overlap", I32), ("graph", I32)]
 
 
 class PfInfo(ctypes.Structure):
@@ -111,7 +111,7 @@ def lib():
 def make_params(pd: dict, cfg: dict | None = None, *, layer_height: float | None = None, T0: float | None = None,
                 aniso: bool | None = None, delta_sl: float | None = None, window: bool | None = None,
                 variant: int = 0, nan_check_every: int = 0, nx: int | None = None, ny: int | None = None,
-                shortcuts: bool = False, overlap: int = 0, no_graph: bool = False) -> PfParams:
+                shortcuts: bool = False, overlap: int = 0, graph: bool = False) -> PfParams:
     """PfParams from a params/*.json dict and (optionally) a configs/*.json dict."""
     p = PfParams()
     p.dx, p.dt, p.eps = pd["dx"], pd["dt"], pd["eps"]
@@ -143,7 +143,7 @@ def make_params(pd: dict, cfg: dict | None = None, *, layer_height: float | None
     p.variant = variant
     p.shortcuts = 1 if shortcuts else 0
     p.overlap = overlap
-    p.no_graph = 1 if no_graph else 0
+    p.graph = 1 if graph else 0
     kinds = {"voronoi": 0, "lamellar": 1, "planar": 2}
     p.init_kind = kinds[ini.get("kind", "voronoi")]
     if "n_seeds" in ini:
