@@ -379,17 +379,20 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
 
 // Opt-in to > 48 KB of dynamic shared memory, once per process (pf_create;
 // not inside a stream capture).
+static int g_mu_slots = 1;   // resident CTAs on the GPU
+
 void prepare_mu_tiled() {
   const int sm = (int)sizeof(MuSmem);
   cudaFuncSetAttribute(mu_tiled_kernel<MU_FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   cudaFuncSetAttribute(mu_tiled_kernel<MU_LOCAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   cudaFuncSetAttribute(mu_tiled_kernel<MU_NEIGHBOR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  g_mu_slots = grid_slots(mu_tiled_kernel<MU_FULL>, NTHR, sm);
 }
 
 template <int MODE>
 void launch_mu_mode(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm) {
   const int gx = (b.nx + TX - 1) / TX, gy = (b.ny + TY - 1) / TY;
-  const int kz = chunk_z(b.nz, gx * gy);
+  const int kz = chunk_z(b.nz, gx * gy, g_mu_slots, 8, true);
   dim3 grd(gx, gy, (b.nz + kz - 1) / kz), blk(TX, TY);
   mu_tiled_kernel<MODE><<<grd, blk, sizeof(MuSmem), s>>>(tm, kp, b, kz);
 }

@@ -248,15 +248,22 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
 
 // Opt-in to > 48 KB of dynamic shared memory, once per process (pf_create;
 // not inside a stream capture).
+static int g_phi_slots[2] = {1, 1};   // resident CTAs on the GPU, [ANISO]
+
 void prepare_phi_tiled() {
   const int sm = (int)sizeof(PhiSmem);
   cudaFuncSetAttribute(phi_tiled_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   cudaFuncSetAttribute(phi_tiled_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  g_phi_slots[0] = grid_slots(phi_tiled_kernel<false>, NTHR, sm);
+  g_phi_slots[1] = grid_slots(phi_tiled_kernel<true>, NTHR, sm);
 }
 
 void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm) {
   const int gx = (b.nx + TX - 1) / TX, gy = (b.ny + TY - 1) / TY;
-  const int kz = chunk_z(b.nz, gx * gy);
+#ifndef PF_PHI_WAVES
+#define PF_PHI_WAVES 16
+#endif
+  const int kz = chunk_z(b.nz, gx * gy, g_phi_slots[kp.aniso ? 1 : 0], PF_PHI_WAVES, false);
   dim3 grd(gx, gy, (b.nz + kz - 1) / kz), blk(TX, TY);
   const size_t sm = sizeof(PhiSmem);
   if (kp.aniso) phi_tiled_kernel<true><<<grd, blk, sm, s>>>(tm, kp, b, kz);
