@@ -182,7 +182,16 @@ __global__ void copy_kernel(const CopyOp *__restrict__ ops, int nops) {
     const uint32_t r = t / ex, x = t - r * ex, z = r / ey, y = r - z * ey;
     const int64_t so = x * op.ssx + y * op.ssy + z * op.ssz;
     const int64_t dof = x * op.dsx + y * op.dsy + z * op.dsz;
-    for (int c = 0; c < op.ncomp; ++c) op.dst[c][dof] = op.src[c][so];
+    if (op.xpad >= 0) {
+      for (int c = 0; c < op.ncomp; ++c) {
+        const double v = op.src[c][so];
+        double2 *sec = reinterpret_cast<double2 *>(op.dst[c] + dof - op.xpad);
+        sec[0] = make_double2(op.xpad == 0 ? v : 0.0, op.xpad == 1 ? v : 0.0);
+        sec[1] = make_double2(op.xpad == 2 ? v : 0.0, op.xpad == 3 ? v : 0.0);
+      }
+    } else {
+      for (int c = 0; c < op.ncomp; ++c) op.dst[c][dof] = op.src[c][so];
+    }
   }
 }
 

@@ -61,6 +61,10 @@ struct CopyOp {
   int ex, ey, ez;           // extents
   int ncomp;
   int64_t cta0;             // first CTA of this op in its launch (upload_ops)
+  int xpad;                 // >= 0: a ghost column alone in its 32-byte sector (the other
+                            // three doubles are row padding) at this slot: each cell is
+                            // written as the whole sector, so DRAM sees no partial-sector
+                            // read-modify-write; -1: plain copy
 };
 constexpr int COPY_CELLS_PER_CTA = 1024;   // 256 threads x 4 cells
 

@@ -208,6 +208,18 @@ int local_index(const pf_ctx *c, int bid) {
   return -1;
 }
 
+// Ghost column of an x-direction region whose 32-byte sector holds no interior
+// cell (the other doubles are row padding): the slot of the ghost in that
+// sector, else -1.  i = -1 sits at column XO-1 = 3, the end of the row's first
+// sector; i = nx at column XO+nx, the start of a sector when nx % 4 == 0.
+int ghost_xpad(const Region &r, int nx) {
+  static_assert(XO == 4, "row padding layout");
+  if (r.ext[0] != 1) return -1;
+  if (r.ds[0] == -1) return 3;
+  if (r.ds[0] == nx && (XO + nx) % 4 == 0) return 0;
+  return -1;
+}
+
 // Upload a copy list; each op gets CTAs in proportion to its size (first CTA
 // in cta0), *nctas = the launch's CTA count: a 12-edge + 6-face halo is then a
 // few thousand CTAs, not 18 x the largest face's.
@@ -350,6 +362,7 @@ pf_status build_plans(pf_ctx *c) {
           }
           op.ssx = op.dsx = 1; op.ssy = op.dsy = B.pitch; op.ssz = op.dsz = B.plane;
           op.ex = (int)r.ext[0]; op.ey = (int)r.ext[1]; op.ez = (int)r.ext[2]; op.ncomp = ncomp;
+          op.xpad = ghost_xpad(r, nx);
           local.push_back(op);
           pl.max_local = std::max<int64_t>(pl.max_local, r.ext[0] * r.ext[1] * r.ext[2]);
         }
@@ -369,6 +382,7 @@ pf_status build_plans(pf_ctx *c) {
           op.ssx = 1; op.ssy = S.pitch; op.ssz = S.plane;
           op.dsx = 1; op.dsy = r.ext[0]; op.dsz = r.ext[0] * r.ext[1];
           op.ex = (int)r.ext[0]; op.ey = (int)r.ext[1]; op.ez = (int)r.ext[2]; op.ncomp = ncomp;
+          op.xpad = -1;
           pack.push_back(op);
           pl.max_pack = std::max(pl.max_pack, n);
           o += n * ncomp;
@@ -386,6 +400,7 @@ pf_status build_plans(pf_ctx *c) {
           op.ssx = 1; op.ssy = r.ext[0]; op.ssz = r.ext[0] * r.ext[1];
           op.dsx = 1; op.dsy = B.pitch; op.dsz = B.plane;
           op.ex = (int)r.ext[0]; op.ey = (int)r.ext[1]; op.ez = (int)r.ext[2]; op.ncomp = ncomp;
+          op.xpad = ghost_xpad(r, nx);
           unpack.push_back(op);
           pl.max_unpack = std::max(pl.max_unpack, n);
           o2 += n * ncomp;
