@@ -1,6 +1,7 @@
 // pf_kernels.cu — per-plane table, naive (reference-variant) sweeps, halo box
 // copies, device initial condition, window front reduction, NaN check and
 // gather/scatter between the padded ghost layout and the public SoA layout.
+#include <algorithm>
 #include <cmath>
 #include "pf_kernels.cuh"
 
@@ -356,21 +357,27 @@ void launch_nancheck(cudaStream_t s, const double *const f[NPH], int ncomp, int 
                                           nx, ny, nz, pitch, plane, d_first);
 }
 
-// gather (padded field -> compact SoA box inside a larger compact array) or scatter
+// gather (padded field -> compact SoA box inside a larger compact array) or
+// scatter.  One CTA per x-row (grid-stride over the ny*nz rows), threads along
+// the row: coalesced on both sides, the index split once per row.
 __global__ void gather_kernel(const double *f0, const double *f1, const double *f2, const double *f3, double *w0,
                               double *w1, double *w2, double *w3, int ncomp, int nx, int ny, int nz, int64_t pitch,
                               int64_t plane, double *dst, int64_t dnx, int64_t dny, int64_t dn, int64_t ox,
                               int64_t oy, int64_t oz, int scatter) {
-  const int64_t n = (int64_t)nx * ny * nz;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t % nx, j = (t / nx) % ny, k = t / ((int64_t)nx * ny);
-    const int64_t o = k * plane + j * pitch + i;
-    const int64_t d = ((oz + k) * dny + (oy + j)) * dnx + (ox + i);
-    const double *fs[4] = {f0, f1, f2, f3};
-    double *ws[4] = {w0, w1, w2, w3};
-    for (int c = 0; c < ncomp; ++c) {
-      if (scatter) ws[c][o] = dst[c * dn + d];
-      else dst[c * dn + d] = fs[c][o];
+  const double *fs[4] = {f0, f1, f2, f3};
+  double *ws[4] = {w0, w1, w2, w3};
+  const int64_t rows = (int64_t)ny * nz;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int64_t j = r % ny, k = r / ny;
+    const int64_t o = k * plane + j * pitch;
+    const int64_t d = ((oz + k) * dny + (oy + j)) * dnx + ox;
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c >= ncomp) break;
+        if (scatter) ws[c][o + i] = dst[c * dn + d + i];
+        else dst[c * dn + d + i] = fs[c][o + i];
+      }
     }
   }
 }
@@ -383,8 +390,10 @@ void launch_gather(cudaStream_t s, const double *const f[NPH], int ncomp, int nx
   if (scatter) for (int c = 0; c < ncomp; ++c) w[c] = fw[c];
   const double *r[4] = {z, z, z, z};
   if (!scatter) for (int c = 0; c < ncomp; ++c) r[c] = f[c];
-  gather_kernel<<<148 * 8, 256, 0, s>>>(r[0], r[1], r[2], r[3], w[0], w[1], w[2], w[3], ncomp, nx, ny, nz, pitch,
-                                        plane, dst, dnx, dny, dn, ox, oy, oz, scatter ? 1 : 0);
+  const int64_t rows = (int64_t)ny * nz;
+  const unsigned grid = (unsigned)std::min<int64_t>(rows, 148 * 16);
+  gather_kernel<<<grid, 256, 0, s>>>(r[0], r[1], r[2], r[3], w[0], w[1], w[2], w[3], ncomp, nx, ny, nz, pitch, plane,
+                                     dst, dnx, dny, dn, ox, oy, oz, scatter ? 1 : 0);
 }
 
 // FP32 checkpoint conversion: one padded binary64 component
@@ -393,19 +402,23 @@ void launch_gather(cudaStream_t s, const double *const f[NPH], int ncomp, int nx
 // float -> double is exact.
 __global__ void cvt32_kernel(double *f, int nx, int ny, int nz, int64_t pitch, int64_t plane, float *dst,
                              int64_t dnx, int64_t dny, int64_t ox, int64_t oy, int64_t oz, int to_fields) {
-  const int64_t n = (int64_t)nx * ny * nz;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t % nx, j = (t / nx) % ny, k = t / ((int64_t)nx * ny);
-    const int64_t o = k * plane + j * pitch + i;
-    const int64_t d = ((oz + k) * dny + (oy + j)) * dnx + (ox + i);
-    if (to_fields) f[o] = (double)dst[d];
-    else dst[d] = __double2float_rn(f[o]);
+  const int64_t rows = (int64_t)ny * nz;   // one CTA per x-row, as gather_kernel
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int64_t j = r % ny, k = r / ny;
+    const int64_t o = k * plane + j * pitch;
+    const int64_t d = ((oz + k) * dny + (oy + j)) * dnx + ox;
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+      if (to_fields) f[o + i] = (double)dst[d + i];
+      else dst[d + i] = __double2float_rn(f[o + i]);
+    }
   }
 }
 
 void launch_cvt32(cudaStream_t s, double *f, int nx, int ny, int nz, int64_t pitch, int64_t plane, float *dst,
                   int64_t dnx, int64_t dny, int64_t ox, int64_t oy, int64_t oz, bool to_fields) {
-  cvt32_kernel<<<148 * 8, 256, 0, s>>>(f, nx, ny, nz, pitch, plane, dst, dnx, dny, ox, oy, oz, to_fields ? 1 : 0);
+  const int64_t rows = (int64_t)ny * nz;
+  const unsigned grid = (unsigned)std::min<int64_t>(rows, 148 * 16);
+  cvt32_kernel<<<grid, 256, 0, s>>>(f, nx, ny, nz, pitch, plane, dst, dnx, dny, ox, oy, oz, to_fields ? 1 : 0);
 }
 
 }  // namespace pf

@@ -75,6 +75,7 @@ struct pf_ctx {
   cudaStream_t cstream = nullptr;
   cudaEvent_t ev_mu_done = nullptr, ev_mu_halo = nullptr;
   cudaEvent_t ev_phi_done = nullptr, ev_phi_halo = nullptr;   // Algorithm 2's phi halo hiding
+  cudaEvent_t ev_copy = nullptr, ev_stage[2] = {nullptr, nullptr};  // pf_read / pf_write staging
   bool mu_pending = false;
   ncclComm_t comm_mu = nullptr;
   double *d_tab = nullptr;
@@ -614,18 +615,30 @@ bool is_device_ptr(const void *p) {
 // copy the rank box between the public compact layout (user, host/device) and the fields
 pf_status move_state(pf_ctx *c, double *phi, double *mu, bool to_fields) {
   const int64_t n = c->box_nx * c->box_ny * c->box_nz;
+  // host buffers: component by component through two device staging buffers,
+  // the PCIe copy of one component (comm stream) overlapping the layout kernel
+  // of the other (main stream)
+  int q_all = 0;
   for (int field = 0; field < 2; ++field) {
     double *user = field == 0 ? phi : mu;
     const int ncomp = field == 0 ? NPH : NMU;
     const bool dev = is_device_ptr(user);
-    if (!dev && !c->d_stage) {  // one component of staging, allocated on first host transfer
+    if (!dev && !c->d_stage) {  // two components of staging, allocated on first host transfer
       c->stage_elems = n;
-      CK(cudaMalloc(&c->d_stage, (size_t)n * sizeof(double)));
+      CK(cudaMalloc(&c->d_stage, 2 * (size_t)n * sizeof(double)));
     }
-    for (int q = 0; q < ncomp; ++q) {  // component by component (bounded staging)
-      double *buf = dev ? user + (int64_t)q * n : c->d_stage;
-      if (to_fields && !dev)
-        CK(cudaMemcpyAsync(buf, user + (int64_t)q * n, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    for (int q = 0; q < ncomp; ++q, ++q_all) {
+      const int sb = q_all & 1;
+      double *buf = dev ? user + (int64_t)q * n : c->d_stage + sb * n;
+      double *hbuf = user + (int64_t)q * n;
+      if (!dev) {   // staging buffer sb free: its previous user (component q_all - 2) is done
+        CK(cudaStreamWaitEvent(to_fields ? c->cstream : c->stream, c->ev_stage[sb], 0));
+      }
+      if (to_fields && !dev) {
+        CK(cudaMemcpyAsync(buf, hbuf, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, c->cstream));
+        CK(cudaEventRecord(c->ev_copy, c->cstream));
+        CK(cudaStreamWaitEvent(c->stream, c->ev_copy, 0));
+      }
       for (const auto &b : c->blocks) {
         double *base = field_ptr(b, field, c->cur, q) + cell_off(b, 0, 0, 0);
         const double *f[NPH] = {base, nullptr, nullptr, nullptr};
@@ -634,10 +647,18 @@ pf_status move_state(pf_ctx *c, double *phi, double *mu, bool to_fields) {
                       b.x0 - c->box_x0, b.y0 - c->box_y0, b.z0 - c->box_z0, to_fields, w);
       }
       CK(cudaGetLastError());
-      if (!to_fields && !dev)
-        CK(cudaMemcpyAsync(user + (int64_t)q * n, buf, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      if (dev) continue;
+      if (to_fields) {
+        CK(cudaEventRecord(c->ev_stage[sb], c->stream));                 // scatter done: buffer free
+      } else {
+        CK(cudaEventRecord(c->ev_copy, c->stream));                      // gather done
+        CK(cudaStreamWaitEvent(c->cstream, c->ev_copy, 0));
+        CK(cudaMemcpyAsync(hbuf, buf, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, c->cstream));
+        CK(cudaEventRecord(c->ev_stage[sb], c->cstream));                // copy-out done: buffer free
+      }
     }
   }
+  CK(cudaStreamSynchronize(c->cstream));
   CK(cudaStreamSynchronize(c->stream));
   return PF_OK;
 }
@@ -920,7 +941,10 @@ pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
       cudaEventCreateWithFlags(&c->ev_mu_done, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_mu_halo, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_phi_done, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_phi_halo, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&c->ev_phi_halo, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_stage[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_stage[1], cudaEventDisableTiming) != cudaSuccess) {
     fail(c, PF_ERR_CUDA, "comm stream / events");
     return bail(PF_ERR_CUDA);
   }
@@ -1405,6 +1429,8 @@ void pf_destroy(pf_ctx *c) {
   if (c->ev_mu_halo) cudaEventDestroy(c->ev_mu_halo);
   if (c->ev_phi_done) cudaEventDestroy(c->ev_phi_done);
   if (c->ev_phi_halo) cudaEventDestroy(c->ev_phi_halo);
+  if (c->ev_copy) cudaEventDestroy(c->ev_copy);
+  for (auto e : c->ev_stage) if (e) cudaEventDestroy(e);
   if (c->cstream) cudaStreamDestroy(c->cstream);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   cudaGetLastError();
