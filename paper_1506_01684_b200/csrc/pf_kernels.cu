@@ -183,15 +183,23 @@ __global__ void copy_kernel(const CopyOp *__restrict__ ops, int nops) {
     const uint32_t r = t / ex, x = t - r * ex, z = r / ey, y = r - z * ey;
     const int64_t so = x * op.ssx + y * op.ssy + z * op.ssz;
     const int64_t dof = x * op.dsx + y * op.dsy + z * op.dsz;
+    // all components' loads first (the source and destination pointers could
+    // alias as far as the compiler knows): four reads in flight per thread
+    double v[NPH];
+#pragma unroll
+    for (int c = 0; c < NPH; ++c) v[c] = c < op.ncomp ? op.src[c][so] : 0.0;
     if (op.xpad >= 0) {
-      for (int c = 0; c < op.ncomp; ++c) {
-        const double v = op.src[c][so];
+#pragma unroll
+      for (int c = 0; c < NPH; ++c) {
+        if (c >= op.ncomp) break;
         double2 *sec = reinterpret_cast<double2 *>(op.dst[c] + dof - op.xpad);
-        sec[0] = make_double2(op.xpad == 0 ? v : 0.0, op.xpad == 1 ? v : 0.0);
-        sec[1] = make_double2(op.xpad == 2 ? v : 0.0, op.xpad == 3 ? v : 0.0);
+        sec[0] = make_double2(op.xpad == 0 ? v[c] : 0.0, op.xpad == 1 ? v[c] : 0.0);
+        sec[1] = make_double2(op.xpad == 2 ? v[c] : 0.0, op.xpad == 3 ? v[c] : 0.0);
       }
     } else {
-      for (int c = 0; c < op.ncomp; ++c) op.dst[c][dof] = op.src[c][so];
+#pragma unroll
+      for (int c = 0; c < NPH; ++c)
+        if (c < op.ncomp) op.dst[c][dof] = v[c];
     }
   }
 }
