@@ -114,6 +114,24 @@ __device__ __forceinline__ void pair_grad_aniso(double g2, double delta, const d
   }
 }
 
+// Component d alone of pair_grad_aniso (the face flux needs only the normal
+// component): the same pinned operations, so bitwise the same value.
+__device__ __forceinline__ double pair_grad_aniso_d(double g2, double delta, const double q[3], int d) {
+  const double q2 = RN_FMA(q[2], q[2], RN_FMA(q[1], q[1], RN_MUL(q[0], q[0])));
+  if (q2 == 0.0) return 0.0;
+  double s2[3];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) s2[e] = RN_MUL(q[e], q[e]);
+  const double s4 = RN_FMA(s2[2], s2[2], RN_FMA(s2[1], s2[1], RN_MUL(s2[0], s2[0])));
+  const double r2 = __drcp_rn(q2);
+  const double r4 = RN_MUL(r2, r2);
+  const double x = RN_MUL(s4, r4);
+  const double ac = RN_SUB(1.0, RN_MUL(delta, RN_FMA(-4.0, x, 3.0)));
+  const double d16 = RN_MUL(16.0, delta);
+  const double t = RN_MUL(RN_FMA(s2[d], q[d], -RN_MUL(RN_MUL(s4, r2), q[d])), r2);
+  return RN_MUL(RN_MUL(g2, ac), RN_FMA(d16, t, RN_MUL(ac, q[d])));
+}
+
 // Face flux j_a (component d) of the phi-sweep between cells lo and hi = lo+e_d
 // (oracle O4.5): phibar = (lo+hi)/2, normal gradient (hi-lo)/dx, tangential
 // gradient = mean of the two centre gradients (anisotropic only);
@@ -155,17 +173,13 @@ __device__ __forceinline__ void phi_face(const KParams &kp, const double plo[NPH
 #pragma unroll
     for (int p = 0; p < 6; ++p) {
       const int a = pair_a(p), b = pair_b(p);
-      double q[3], g[3];
+      double q[3];
 #pragma unroll
       for (int e = 0; e < 3; ++e) q[e] = RN_FMA(pb[a], gf[b][e], -RN_MUL(pb[b], gf[a][e]));
-      if (kp.delta[p] == 0.0) {
-#pragma unroll
-        for (int e = 0; e < 3; ++e) g[e] = RN_MUL(kp.g2[p], q[e]);
-      } else {
-        pair_grad_aniso(kp.g2[p], kp.delta[p], q, g);
-      }
-      jf[a] = RN_FMA(-g[d], pb[b], jf[a]);
-      jf[b] = RN_FMA(g[d], pb[a], jf[b]);
+      // only the normal component g_d of the pair gradient enters the flux
+      const double gd = kp.delta[p] == 0.0 ? RN_MUL(kp.g2[p], q[d]) : pair_grad_aniso_d(kp.g2[p], kp.delta[p], q, d);
+      jf[a] = RN_FMA(-gd, pb[b], jf[a]);
+      jf[b] = RN_FMA(gd, pb[a], jf[b]);
     }
   }
 }
