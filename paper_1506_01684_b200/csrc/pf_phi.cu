@@ -127,6 +127,10 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
     const int fb = (k - k0) & 1;
     // D: faces of plane k; own column values to registers
     double pm[NPH], pc[NPH], pp[NPH], jzp[NPH];
+    // anisotropic: the own cell's centre gradients once (the hi side of its
+    // -x / -y faces and the cell update's gradients; pinned cgrad: same bits)
+    double gown[NPH][3];
+    if (ANISO) tan_grad(sc, sm, sp, oc, orow, -1, gown);
     {
       double jf[NPH], lo[NPH], hi[NPH], gl[NPH][3], gh[NPH][3];
 #pragma unroll
@@ -136,7 +140,10 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
         for (int a = 0; a < NPH; ++a) { lo[a] = T(S.p[sc][a], lr, lc); hi[a] = T(S.p[sc][a], orow, oc); }
         if (ANISO) {
           tan_grad(sc, sm, sp, lc, lr, d, gl);
-          tan_grad(sc, sm, sp, oc, orow, d, gh);
+#pragma unroll
+          for (int a = 0; a < NPH; ++a)
+#pragma unroll
+            for (int e = 0; e < 3; ++e) gh[a][e] = gown[a][e];
         }
         phi_face(kp, lo, hi, ANISO ? gl : gdum, ANISO ? gh : gdum, d, jf);
 #pragma unroll
@@ -170,11 +177,8 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
         pc[a] = T(S.p[sc][a], orow, oc);
         pp[a] = T(S.p[sp][a], orow, oc);
       }
-      if (ANISO) {
-        tan_grad(sc, sc, sc, oc, orow, 2, gl);
-        tan_grad(sp, sp, sp, oc, orow, 2, gh);
-      }
-      phi_face(kp, pc, pp, ANISO ? gl : gdum, ANISO ? gh : gdum, 2, jzp);
+      if (ANISO) tan_grad(sp, sp, sp, oc, orow, 2, gh);   // lo side: the own cell's gown
+      phi_face(kp, pc, pp, ANISO ? gown : gdum, ANISO ? gh : gdum, 2, jzp);
     }
     // region shortcut (NEXT-1): a warp whose cells
     // are all simplex vertices with an identical D3C7 (D3C19) neighbourhood
@@ -221,14 +225,7 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
       for (int a = 0; a < NPH; ++a) b.out[a][o] = pc[a];
     } else if (active) {
       if (ANISO) {
-        double gc[NPH][3];
-#pragma unroll
-        for (int a = 0; a < NPH; ++a) {
-          gc[a][0] = cgrad(kp, T(S.p[sc][a], orow, oc - 1), T(S.p[sc][a], orow, oc + 1));
-          gc[a][1] = cgrad(kp, T(S.p[sc][a], orow - 1, oc), T(S.p[sc][a], orow + 1, oc));
-          gc[a][2] = cgrad(kp, pm[a], pp[a]);
-        }
-        phi_cell_rhs0(kp, S.tab[sc], pc, mu_c, gc, r0);
+        phi_cell_rhs0(kp, S.tab[sc], pc, mu_c, gown, r0);
       }
       double dsum[NPH], out[NPH];
 #pragma unroll
