@@ -33,7 +33,7 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=(),
-          csrc: str | None = None, extra_sources=(), nccl: bool = True) -> str:
+          csrc: str | None = None, extra_sources=(), nccl: bool = True, extra_flags=()) -> str:
     """Compile libpf.so; `out`/`defines`/`csrc` build an alternative copy for A/B timing (tools/);
     `extra_sources` + nccl=False link a test stand-in instead of libnccl (tests/fakenccl)."""
     if out is None and not force and not needs_build():
@@ -43,7 +43,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
            "-I", inc, "-I", os.path.join(os.path.dirname(HERE), "include"),
-           *[f"-D{d}" for d in defines],
+           *[f"-D{d}" for d in defines], *extra_flags,
            "-o", out or LIB] + [os.path.join(src, f) for f in SOURCES] + list(extra_sources) + \
           (["-L", libdir, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + libdir] if nccl else [])
     subprocess.check_call(cmd)

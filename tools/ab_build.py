@@ -11,7 +11,8 @@ from paper_1506_01684_b200 import build as B
 
 name, rest = sys.argv[1], sys.argv[2:]
 defs = [a[2:] for a in rest if a.startswith("-D")]
-revs = [a for a in rest if not a.startswith("-D")]
+flags = [a[2:] for a in rest if a.startswith("-F")]          # -F<nvcc flag>, e.g. -F-Xptxas=-foo
+revs = [a for a in rest if not a.startswith("-D") and not a.startswith("-F")]
 src = None
 if revs:
     base = os.path.join(ROOT, "build", "ab")
@@ -25,5 +26,5 @@ if revs:
                               capture_output=True, check=True).stdout
         open(os.path.join(src, f), "wb").write(blob)
 out = os.path.join(ROOT, "build", f"libpf_{name}.so")
-B.build(out=out, defines=defs, csrc=src)
+B.build(out=out, defines=defs, csrc=src, extra_flags=flags)
 print(out)
