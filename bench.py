@@ -143,7 +143,8 @@ def cpu_oracle_sample(name: str, steps: int, nz_slab: int = 16):
     lh = cfg["init"]["layer_height"]
     nx, ny = min(cfg["nx"], 512), min(cfg["ny"], 512)
     spec = gen.spec_from_config(cfg, cfg["nx"], cfg["ny"])
-    z0 = int(lh) - nz_slab // 2
+    nz_slab = min(nz_slab, cfg["nz"])
+    z0 = max(0, min(int(lh) - nz_slab // 2, cfg["nz"] - nz_slab))
     phi, mu = gen.generate(spec, cfg["nx"], cfg["ny"], cfg["nz"], box=(0, 0, z0, nx, ny, nz_slab))
     p = O.make_params(pd, layer_height=lh - z0, aniso=cfg.get("aniso", False), delta_sl=cfg.get("delta_sl"))
     t0 = time.perf_counter()
@@ -364,8 +365,9 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--graph", action="store_true", help="replay each step as a CUDA graph (single rank)")
-    ap.add_argument("--config", default=CONFIG, choices=["c4", "c5"],
-                    help="c4: weak scaling 512^3 per GPU (default, the headline); c5: strong scaling 1024^3, anisotropic")
+    ap.add_argument("--config", default=CONFIG, choices=["c1", "c2", "c3", "c4", "c5"],
+                    help="c4: weak scaling 512^3 per GPU (default, the headline); c5: strong scaling 1024^3, "
+                         "anisotropic; c1-c3: the single-GPU parity configs")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
