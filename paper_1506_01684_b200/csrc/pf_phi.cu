@@ -25,6 +25,8 @@ struct __align__(128) PhiSmem {
   double fx[2][NPH][TY][TX + 1];   // x-face fluxes at i - 1/2, i = 0..TX (plane parity)
   double fy[2][NPH][TY + 1][TX];   // y-face fluxes at j - 1/2, j = 0..TY
   uint64_t bar[NSLOT];             // one mbarrier per slot
+  double jz[NPH][TY][TX];          // anisotropic: the z-face carry, thread-private (measured: frees
+                                   // registers the D3C19 faces use; isotropic keeps it in registers)
 };
 
 constexpr uint32_t PHI_STAGE_BYTES = (NPH * RXS * RY + TAB) * 8;
@@ -101,6 +103,9 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
       tan_grad(s1, s1, s1, oc, orow, 2, gh);
     }
     phi_face(kp, lo, hi, ANISO ? gl : gdum, ANISO ? gh : gdum, 2, jzm);
+    if (ANISO)
+#pragma unroll
+      for (int a = 0; a < NPH; ++a) S.jz[a][ty][tx] = jzm[a];
   }
 
   // One CTA barrier per plane (B): the face buffers alternate by plane parity,
@@ -231,14 +236,17 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
 #pragma unroll
       for (int a = 0; a < NPH; ++a)
         dsum[a] = ((S.fx[fb][a][ty][tx + 1] - S.fx[fb][a][ty][tx]) + (S.fy[fb][a][ty + 1][tx] - S.fy[fb][a][ty][tx])) +
-                  (jzp[a] - jzm[a]);
+                  (jzp[a] - (ANISO ? S.jz[a][ty][tx] : jzm[a]));
       phi_cell_finish(kp, S.tab[sc], pc, r0, dsum, out);
       const int64_t o = (int64_t)k * b.plane + colo;
 #pragma unroll
       for (int a = 0; a < NPH; ++a) b.out[a][o] = out[a];
     }
 #pragma unroll
-    for (int a = 0; a < NPH; ++a) jzm[a] = jzp[a];
+    for (int a = 0; a < NPH; ++a) {
+      if (ANISO) S.jz[a][ty][tx] = jzp[a];
+      else jzm[a] = jzp[a];
+    }
   }
 #undef T
 }
