@@ -108,11 +108,15 @@ def load_cfg(name):
     return json.load(open(os.path.join(ROOT, "configs", f"{name}.json")))
 
 
-def workload(name: str, world: int):
+def workload(name: str, world: int, grid=None):
     """Global grid, block grid and per-rank cells of a config at `world` ranks:
-    weak scaling (per-GPU block, C4) or strong scaling (fixed global grid, C5)."""
+    weak scaling (per-GPU block, C4) or strong scaling (fixed global grid, C5);
+    `grid` overrides the global grid (e.g. C5's 1024x1024x256 slab, reading A22)."""
     from paper_1506_01684_b200 import dist as pdist
     cfg = load_cfg(name)
+    if grid:
+        cfg = dict(cfg, nx=grid[0], ny=grid[1], nz=grid[2], per_gpu=False)
+        return cfg, tuple(grid), pdist.decomposition(world, name), grid[0] * grid[1] * grid[2] // world, "strong"
     if cfg.get("per_gpu"):
         (NX, NY, NZ), blocks = pdist.weak_grid(world, per=cfg["nx"], config=name)
         scaling = "weak"
@@ -175,7 +179,7 @@ def run_reference(args):
         return 0
     steps, warm = args.steps, args.warmup
     world = _env_int("WORLD_SIZE", 1)
-    cfg, grid, blocks, cells_local, scaling = workload(args.config, world)
+    cfg, grid, blocks, cells_local, scaling = workload(args.config, world, args.grid)
     # each step: one oracle step over a bounded sample of the workload
     if warm:
         cpu_oracle_sample(args.config, 1, nz_slab=16)
@@ -204,7 +208,7 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
-    cfg, (NX, NY, NZ), (px, py, pz), cells_local, scaling = workload(args.config, world)
+    cfg, (NX, NY, NZ), (px, py, pz), cells_local, scaling = workload(args.config, world, args.grid)
     from inputs import gen
     pd = gen.load_params("v1")
     prm = pf.make_params(pd, cfg, nx=NX, ny=NY, nan_check_every=0, graph=args.graph)
@@ -365,6 +369,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--graph", action="store_true", help="replay each step as a CUDA graph (single rank)")
+    ap.add_argument("--grid", type=int, nargs=3, metavar=("NX", "NY", "NZ"),
+                    help="global grid overriding the config's (its physics and init recipe kept)")
     ap.add_argument("--config", default=CONFIG, choices=["c1", "c2", "c3", "c4", "c5"],
                     help="c4: weak scaling 512^3 per GPU (default, the headline); c5: strong scaling 1024^3, "
                          "anisotropic; c1-c3: the single-GPU parity configs")
