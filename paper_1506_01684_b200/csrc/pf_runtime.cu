@@ -48,9 +48,10 @@ struct Block {
 };
 
 struct Plan {                // halo plan of one field in one copy
-  CopyOp *d_local = nullptr, *d_pack = nullptr, *d_unpack = nullptr;
-  int nlocal = 0, npack = 0, nunpack = 0;
-  int64_t max_local = 0, max_pack = 0, max_unpack = 0;   // after upload: CTAs of the local / unpack launches
+  CopyOp *d_local = nullptr;   // pack into the send buffer + local copies (one launch)
+  CopyOp *d_unpack = nullptr;  // unpack from the receive buffer (one launch, after the exchange)
+  int nlocal = 0, nunpack = 0;
+  int64_t ctas_local = 0, ctas_unpack = 0;   // CTAs of the two launches (upload_ops)
 };
 
 struct Peer {
@@ -348,7 +349,6 @@ pf_status build_plans(pf_ctx *c) {
     for (int copy = 0; copy < 2; ++copy) {
       std::vector<CopyOp> local, pack, unpack;
       Plan &pl = c->plan[field][copy];
-      pl.max_local = pl.max_pack = pl.max_unpack = 0;
       // local copies: both ends on this rank
       for (size_t q = 0; q < c->blocks.size(); ++q) {
         const Block &B = c->blocks[q];
@@ -365,7 +365,6 @@ pf_status build_plans(pf_ctx *c) {
           op.ex = (int)r.ext[0]; op.ey = (int)r.ext[1]; op.ez = (int)r.ext[2]; op.ncomp = ncomp;
           op.xpad = ghost_xpad(r, nx);
           local.push_back(op);
-          pl.max_local = std::max<int64_t>(pl.max_local, r.ext[0] * r.ext[1] * r.ext[2]);
         }
       }
       // pack: regions this rank sends, per peer in the receiver's order
@@ -385,7 +384,6 @@ pf_status build_plans(pf_ctx *c) {
           op.ex = (int)r.ext[0]; op.ey = (int)r.ext[1]; op.ez = (int)r.ext[2]; op.ncomp = ncomp;
           op.xpad = -1;
           pack.push_back(op);
-          pl.max_pack = std::max(pl.max_pack, n);
           o += n * ncomp;
         }
         int64_t o2 = p.recv_off;
@@ -403,7 +401,6 @@ pf_status build_plans(pf_ctx *c) {
           op.ex = (int)r.ext[0]; op.ey = (int)r.ext[1]; op.ez = (int)r.ext[2]; op.ncomp = ncomp;
           op.xpad = ghost_xpad(r, nx);
           unpack.push_back(op);
-          pl.max_unpack = std::max(pl.max_unpack, n);
           o2 += n * ncomp;
         }
       }
@@ -411,10 +408,9 @@ pf_status build_plans(pf_ctx *c) {
       std::vector<CopyOp> first = pack;
       first.insert(first.end(), local.begin(), local.end());
       pl.nlocal = (int)first.size();
-      pl.max_local = std::max(pl.max_local, pl.max_pack);
-      CKS(upload_ops(c, first, &pl.d_local, &pl.max_local));
+      CKS(upload_ops(c, first, &pl.d_local, &pl.ctas_local));
       pl.nunpack = (int)unpack.size();
-      CKS(upload_ops(c, unpack, &pl.d_unpack, &pl.max_unpack));
+      CKS(upload_ops(c, unpack, &pl.d_unpack, &pl.ctas_unpack));
     }
   }
   return PF_OK;
@@ -451,7 +447,7 @@ pf_status exchange(pf_ctx *c, int field, int copy, bool overlap = false) {
   cudaStream_t st = overlap ? c->cstream : c->stream;
   ncclComm_t comm = overlap ? c->comm_mu : c->comm;
   TimedSpan ts(c, overlap ? -1 : 2, 0);
-  if (pl.nlocal) { launch_copy(st, pl.d_local, pl.nlocal, pl.max_local); c->launches++; }
+  if (pl.nlocal) { launch_copy(st, pl.d_local, pl.nlocal, pl.ctas_local); c->launches++; }
   if (c->g.nranks > 1 && !c->peers[field].empty()) {
     CKN(ncclGroupStart());
     for (const Peer &p : c->peers[field]) {
@@ -460,7 +456,7 @@ pf_status exchange(pf_ctx *c, int field, int copy, bool overlap = false) {
     }
     CKN(ncclGroupEnd());
   }
-  if (pl.nunpack) { launch_copy(st, pl.d_unpack, pl.nunpack, pl.max_unpack); c->launches++; }
+  if (pl.nunpack) { launch_copy(st, pl.d_unpack, pl.nunpack, pl.ctas_unpack); c->launches++; }
   CK(cudaGetLastError());
   return PF_OK;
 }
