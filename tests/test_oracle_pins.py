@@ -699,3 +699,27 @@ def test_committed_flop_counts_match_oracle():
         ref = O.count_flops(O.make_params(pd, layer_height=cfg["init"]["layer_height"], aniso=cfg.get("aniso", False),
                                           delta_sl=cfg.get("delta_sl")))
         assert {k: int(v) for k, v in ref.items()} == fl, name
+
+
+def test_p17_window_transparency_within_light_cone(pv1):
+    # O7 / reading A16 pinned against "the same physics in a taller box": a
+    # window run (the front forced past 2/3 height so it shifts) equals, bit for
+    # bit, a non-windowed run of a taller domain on the planes that neither the
+    # bottom ghost nor the liquid fill can reach in M steps (the stencil of one
+    # step reaches 2 planes: the mu-sweep reads phi^{n+1}, which read phi^n)
+    from inputs import gen
+    cfg = gen.load_config("c2")
+    nx, ny, nz, extra, M = 12, 12, 48, 6, 6
+    spec = gen.spec_from_config(cfg, nx, ny)
+    spec.layer_height, spec.n_seeds = 33.5, 4
+    tall_phi, tall_mu = gen.generate(spec, nx, ny, nz + extra)
+    p = O.make_params(pv1, layer_height=33.5)
+    shifts = []
+    wphi, wmu, zorig = O.run(p, tall_phi[:, :nz], tall_mu[:, :nz], M, window_on=True, shifts=shifts)
+    tphi, tmu, _ = O.run(p, tall_phi, tall_mu, M)
+    assert zorig == len(shifts) >= 1
+    lo, hi = 2 * M + 1, nz - 2 * M - 1
+    assert np.array_equal(wphi[:, lo:hi], tphi[:, lo + zorig:hi + zorig])
+    assert np.array_equal(wmu[:, lo:hi], tmu[:, lo + zorig:hi + zorig])
+    # and the shift really moved the data: without the origin offset they differ
+    assert not np.array_equal(wphi[:, lo:hi], tphi[:, lo:hi])
