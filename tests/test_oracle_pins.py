@@ -723,3 +723,22 @@ def test_p17_window_transparency_within_light_cone(pv1):
     assert np.array_equal(wmu[:, lo:hi], tmu[:, lo + zorig:hi + zorig])
     # and the shift really moved the data: without the origin offset they differ
     assert not np.array_equal(wphi[:, lo:hi], tphi[:, lo:hi])
+
+
+@pytest.mark.parametrize("aniso", [False, True])
+def test_p18_mirror_symmetry(pv1, aniso):
+    # the step commutes with the mirrors x -> -x and y -> -y (periodic axes; the
+    # cubic anisotropy is mirror-symmetric): catches a face flux or gradient
+    # taken from the wrong side in one direction, which x<->y swaps (P13) miss
+    cfg = gen.load_config("c5" if aniso else "c2")
+    spec = gen.spec_from_config(cfg, 12, 10)
+    spec.layer_height, spec.n_seeds, spec.mu_noise = 6, 5, 1e-2
+    phi, mu = gen.generate(spec, 12, 10, 12)
+    p = _params(pv1, layer_height=7, aniso=aniso, delta_sl=0.05 if aniso else None)
+    a, ma, _ = O.run(p, phi, mu, 10)
+    assert np.abs(a - phi).max() > 1e-3
+    for axis in (3, 2):          # x, y
+        mr = lambda x: np.ascontiguousarray(np.flip(x, axis=axis))   # i -> N-1-i
+        b, mb, _ = O.run(p, mr(phi), mr(mu), 10)
+        assert np.abs(mr(b) - a).max() <= 1e-14, axis
+        assert np.abs(mr(mb) - ma).max() <= 1e-14, axis
