@@ -205,6 +205,8 @@ __device__ __forceinline__ void phi_cell_rhs0(const KParams &kp, const double *_
 __device__ __forceinline__ void phi_cell_finish(const KParams &kp, const double *__restrict__ tab,
                                                 const double ph[NPH], const double r0[NPH],
                                                 const double dsum[NPH], double out[NPH]);
+__device__ __forceinline__ void phi_cell_project(const KParams &kp, const double ph[NPH], const double rhs[NPH],
+                                                 double out[NPH]);
 __device__ __forceinline__ void phi_cell_update_div(const KParams &kp, const double *__restrict__ tab,
                                                     const double ph[NPH], const double mu[NMU],
                                                     const double gc[NPH][3], const double dsum[NPH],
@@ -317,6 +319,13 @@ __device__ __forceinline__ void phi_cell_finish(const KParams &kp, const double 
   double rhs[NPH];
 #pragma unroll
   for (int a = 0; a < NPH; ++a) rhs[a] = r0[a] - epsTdx * dsum[a];
+  phi_cell_project(kp, ph, rhs, out);
+}
+
+// O4.9-4.11 given the right-hand side rhs_a (r0_a minus the scaled face
+// divergence): Lagrange mean, Euler step, simplex projection.
+__device__ __forceinline__ void phi_cell_project(const KParams &kp, const double ph[NPH], const double rhs[NPH],
+                                                 double out[NPH]) {
   const double mean = 0.25 * ((rhs[0] + rhs[1]) + (rhs[2] + rhs[3]));
   double x[NPH];
 #pragma unroll

@@ -130,8 +130,17 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
     wait(k + 1);
     const int sc = slot(k), sm = slot(k - 1), sp = slot(k + 1);
     const int fb = (k - k0) & 1;
-    // D: faces of plane k; own column values to registers
-    double pm[NPH], pc[NPH], pp[NPH], jzp[NPH];
+    // D: faces of plane k.  The own column's values are read from shared memory
+    // once (the LSU pipe, not the FP64 pipe, was the busier one: ncu v14 72 %
+    // vs 58 %) and, isotropic, the cell's own faces enter its divergence from
+    // registers before the barrier:
+    //   dpart = (jz+ - jz-) - jx- - jy-,   rhs = (r0 - c dpart) - c (jx+ + jy+)
+    // with c = eps T / dx (the oracle's O4.6 sum in another order: equal up to
+    // rounding; the anisotropic kernel forms dpart after the barrier).
+    double pc[NPH], pp[NPH], jzp[NPH], dpart[NPH];
+    if (!ANISO)
+#pragma unroll
+      for (int a = 0; a < NPH; ++a) pc[a] = T(S.p[sc][a], orow, oc);
     // anisotropic: the own cell's centre gradients once (the hi side of its
     // -x / -y faces and the cell update's gradients; pinned cgrad: same bits)
     double gown[NPH][3];
@@ -142,19 +151,17 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
       for (int d = 0; d < 2; ++d) {   // own -x (d = 0) and -y (d = 1) face
         const int lc = d == 0 ? oc - 1 : oc, lr = d == 0 ? orow : orow - 1;
 #pragma unroll
-        for (int a = 0; a < NPH; ++a) { lo[a] = T(S.p[sc][a], lr, lc); hi[a] = T(S.p[sc][a], orow, oc); }
-        if (ANISO) {
-          tan_grad(sc, sm, sp, lc, lr, d, gl);
-#pragma unroll
-          for (int a = 0; a < NPH; ++a)
-#pragma unroll
-            for (int e = 0; e < 3; ++e) gh[a][e] = gown[a][e];
+        for (int a = 0; a < NPH; ++a) {
+          lo[a] = T(S.p[sc][a], lr, lc);
+          hi[a] = ANISO ? T(S.p[sc][a], orow, oc) : pc[a];   // anisotropic: re-read (registers)
         }
-        phi_face(kp, lo, hi, ANISO ? gl : gdum, ANISO ? gh : gdum, d, jf);
+        if (ANISO) tan_grad(sc, sm, sp, lc, lr, d, gl);
+        phi_face(kp, lo, hi, ANISO ? gl : gdum, ANISO ? gown : gdum, d, jf);
 #pragma unroll
         for (int a = 0; a < NPH; ++a) {
           if (d == 0) S.fx[fb][a][ty][tx] = jf[a];
           else S.fy[fb][a][ty][tx] = jf[a];
+          if (!ANISO) dpart[a] = d == 0 ? -jf[a] : dpart[a] - jf[a];
         }
       }
       // far faces: +y of the last row (warp 0), +x of the last column (warp 1)
@@ -178,12 +185,17 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
       // z-face k+1/2 (own column)
 #pragma unroll
       for (int a = 0; a < NPH; ++a) {
-        pm[a] = T(S.p[sm][a], orow, oc);
-        pc[a] = T(S.p[sc][a], orow, oc);
         pp[a] = T(S.p[sp][a], orow, oc);
+        if (ANISO) pc[a] = T(S.p[sc][a], orow, oc);
       }
       if (ANISO) tan_grad(sp, sp, sp, oc, orow, 2, gh);   // lo side: the own cell's gown
       phi_face(kp, pc, pp, ANISO ? gown : gdum, ANISO ? gh : gdum, 2, jzp);
+#pragma unroll
+      for (int a = 0; a < NPH; ++a) {
+        if (ANISO) continue;   // anisotropic: formed after the barrier (registers)
+        dpart[a] += jzp[a] - jzm[a];
+        jzm[a] = jzp[a];
+      }
     }
     // region shortcut (NEXT-1): a warp whose cells
     // are all simplex vertices with an identical D3C7 (D3C19) neighbourhood
@@ -195,7 +207,8 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
       for (int a = 0; a < NPH; ++a) {
         const double v = pc[a];
         mine = mine && T(S.p[sc][a], orow, oc - 1) == v && T(S.p[sc][a], orow, oc + 1) == v &&
-               T(S.p[sc][a], orow - 1, oc) == v && T(S.p[sc][a], orow + 1, oc) == v && pm[a] == v && pp[a] == v;
+               T(S.p[sc][a], orow - 1, oc) == v && T(S.p[sc][a], orow + 1, oc) == v &&
+               T(S.p[sm][a], orow, oc) == v && pp[a] == v;
         if (ANISO)
           mine = mine && T(S.p[sc][a], orow - 1, oc - 1) == v && T(S.p[sc][a], orow - 1, oc + 1) == v &&
                  T(S.p[sc][a], orow + 1, oc - 1) == v && T(S.p[sc][a], orow + 1, oc + 1) == v &&
@@ -209,18 +222,21 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
     bool skip = ANISO ? false : bulk_warp();
     // isotropic: the cell terms that need no face flux (phi_cell_rhs0, on the
     // raw centre differences) are formed before the barrier, where the tile
-    // values are still in registers; the anisotropic kernel has no registers
-    // to spare for that and forms them after it
-    double r0[NPH];
+    // values are still at hand; the anisotropic kernel has no registers to
+    // spare for that and forms them after it
+    double q[NPH];   // r0 - c dpart
     if (!ANISO && active && !skip) {
-      double gc[NPH][3];
+      double r0[NPH], gc[NPH][3];
 #pragma unroll
       for (int a = 0; a < NPH; ++a) {
         gc[a][0] = T(S.p[sc][a], orow, oc + 1) - T(S.p[sc][a], orow, oc - 1);
         gc[a][1] = T(S.p[sc][a], orow + 1, oc) - T(S.p[sc][a], orow - 1, oc);
-        gc[a][2] = pp[a] - pm[a];
+        gc[a][2] = pp[a] - T(S.p[sm][a], orow, oc);
       }
       phi_cell_rhs0(kp, S.tab[sc], pc, mu_c, gc, r0);
+      const double c = S.tab[sc][T_EPSTDX];
+#pragma unroll
+      for (int a = 0; a < NPH; ++a) q[a] = r0[a] - c * dpart[a];
     }
     __syncthreads();  // B: faces of plane k complete
     if (ANISO) skip = bulk_warp();
@@ -229,24 +245,27 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
 #pragma unroll
       for (int a = 0; a < NPH; ++a) b.out[a][o] = pc[a];
     } else if (active) {
+      const double c = S.tab[sc][T_EPSTDX];
       if (ANISO) {
+        double r0[NPH];
         phi_cell_rhs0(kp, S.tab[sc], pc, mu_c, gown, r0);
-      }
-      double dsum[NPH], out[NPH];
 #pragma unroll
-      for (int a = 0; a < NPH; ++a)
-        dsum[a] = ((S.fx[fb][a][ty][tx + 1] - S.fx[fb][a][ty][tx]) + (S.fy[fb][a][ty + 1][tx] - S.fy[fb][a][ty][tx])) +
-                  (jzp[a] - (ANISO ? S.jz[a][ty][tx] : jzm[a]));
-      phi_cell_finish(kp, S.tab[sc], pc, r0, dsum, out);
+        for (int a = 0; a < NPH; ++a) {
+          dpart[a] = (jzp[a] - S.jz[a][ty][tx]) - S.fx[fb][a][ty][tx] - S.fy[fb][a][ty][tx];
+          q[a] = r0[a] - c * dpart[a];
+        }
+      }
+      double rhs[NPH], out[NPH];
+#pragma unroll
+      for (int a = 0; a < NPH; ++a) rhs[a] = q[a] - c * (S.fx[fb][a][ty][tx + 1] + S.fy[fb][a][ty + 1][tx]);
+      phi_cell_project(kp, pc, rhs, out);
       const int64_t o = (int64_t)k * b.plane + colo;
 #pragma unroll
       for (int a = 0; a < NPH; ++a) b.out[a][o] = out[a];
     }
+    if (ANISO)
 #pragma unroll
-    for (int a = 0; a < NPH; ++a) {
-      if (ANISO) S.jz[a][ty][tx] = jzp[a];
-      else jzm[a] = jzp[a];
-    }
+      for (int a = 0; a < NPH; ++a) S.jz[a][ty][tx] = jzp[a];   // thread-private slot
   }
 #undef T
 }
