@@ -193,7 +193,9 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
     stage_pn(k0 + 1);
     stage_pm(k0);
   }
-  double fzm[NMU], po_n[NPH], mu_n[NMU];
+  // Mown: the own column's mobility at plane k, carried from the z-face
+  // k-1/2 where it was formed as the upper cell's (same pinned mob2: same bits)
+  double fzm[NMU], po_n[NPH], mu_n[NMU], Mown[NMU];
   {  // z-face k0 - 1/2 from the own column's register quantities at k0-1 and k0
     double pom[NPH], mum[NMU];
     own_load(k0 - 1, pom, mum);
@@ -204,6 +206,8 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
     MuQ qm, qc;
     own_q(k0 - 1, pom, mum, qm);
     own_q(k0, po_n, mu_n, qc);
+    Mown[0] = qc.M[0];
+    Mown[1] = qc.M[1];
     if (MODE == MU_LOCAL) {
 #pragma unroll
       for (int c = 0; c < NMU; ++c) fzm[c] = mu_flux_diff(kp, qm.M[c], qc.M[c], qm.mu[c], qc.mu[c]);
@@ -236,15 +240,11 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
     for (int c = 0; c < NMU; ++c) mu_c[c] = mu_n[c];
     own_load(k + 1, po_n, mu_n);
     mbar_wait(&S.bar_pm[s2], par2(k));   // phi^n / mu of plane k resident
-    if (MODE != MU_NEIGHBOR) {  // mobility of plane k (own + ring cells)
-      double po[NPH];
-#pragma unroll
-      for (int a = 0; a < NPH; ++a) po[a] = T(S.po[s2][a], orow, oc);
-      double M[NMU];
-      mob2(S.tab[sn], po, M);
-      S.M[0][orow][oc] = M[0];
-      S.M[1][orow][oc] = M[1];
+    if (MODE != MU_NEIGHBOR) {  // mobility of plane k (own: carried; ring cells)
+      S.M[0][orow][oc] = Mown[0];
+      S.M[1][orow][oc] = Mown[1];
       if (ring_thr && !rcorner) {
+        double po[NPH], M[NMU];
 #pragma unroll
         for (int a = 0; a < NPH; ++a) po[a] = T(S.po[s2][a], rrow, rcol);
         mob2(S.tab[sn], po, M);
@@ -264,7 +264,8 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
     const bool fast_z = MODE == MU_LOCAL || ((flc & flp) & 1u) || ((flc & flp) & 2u);
     flm = flc;
     flc = flp;
-    // D: faces of plane k
+    // D: faces of plane k; the own -x / -y faces also stay in registers (fxo, fyo)
+    double fxo[NMU] = {0.0, 0.0}, fyo[NMU] = {0.0, 0.0};
     if (fast_xy && MODE == MU_NEIGHBOR) {   // J = 0 on every x/y face of the plane
 #pragma unroll
       for (int c = 0; c < NMU; ++c) {
@@ -280,10 +281,11 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
       }
     } else if (fast_xy) {
 #pragma unroll
-      for (int c = 0; c < NMU; ++c) {
-        const double mc = T(S.mu[s2][c], orow, oc), Mc = S.M[c][orow][oc];
-        S.fx[c][ty][tx] = mu_flux_diff(kp, S.M[c][orow][oc - 1], Mc, T(S.mu[s2][c], orow, oc - 1), mc);
-        S.fy[c][ty][tx] = mu_flux_diff(kp, S.M[c][orow - 1][oc], Mc, T(S.mu[s2][c], orow - 1, oc), mc);
+      for (int c = 0; c < NMU; ++c) {   // own mu, M from registers (inb: the staged values)
+        fxo[c] = mu_flux_diff(kp, S.M[c][orow][oc - 1], Mown[c], T(S.mu[s2][c], orow, oc - 1), mu_c[c]);
+        fyo[c] = mu_flux_diff(kp, S.M[c][orow - 1][oc], Mown[c], T(S.mu[s2][c], orow - 1, oc), mu_c[c]);
+        S.fx[c][ty][tx] = fxo[c];
+        S.fy[c][ty][tx] = fyo[c];
       }
       if (tid < TX + TY) {
         const int d = tid < TX ? 1 : 0;
@@ -302,18 +304,18 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
       {  // own -x face
         RawQ lo = rawq(k, oc - 1, orow), hi = rawq(k, oc, orow);
         lo.Mv[0] = S.M[0][orow][oc - 1]; lo.Mv[1] = S.M[1][orow][oc - 1];
-        hi.Mv[0] = S.M[0][orow][oc]; hi.Mv[1] = S.M[1][orow][oc];
-        mu_face_t<MODE == MU_FULL>(kp, lo, hi, 0, f);
-        S.fx[0][ty][tx] = f[0];
-        S.fx[1][ty][tx] = f[1];
+        hi.Mv[0] = Mown[0]; hi.Mv[1] = Mown[1];
+        mu_face_t<MODE == MU_FULL>(kp, lo, hi, 0, fxo);
+        S.fx[0][ty][tx] = fxo[0];
+        S.fx[1][ty][tx] = fxo[1];
       }
       {  // own -y face
         RawQ lo = rawq(k, oc, orow - 1), hi = rawq(k, oc, orow);
         lo.Mv[0] = S.M[0][orow - 1][oc]; lo.Mv[1] = S.M[1][orow - 1][oc];
-        hi.Mv[0] = S.M[0][orow][oc]; hi.Mv[1] = S.M[1][orow][oc];
-        mu_face_t<MODE == MU_FULL>(kp, lo, hi, 1, f);
-        S.fy[0][ty][tx] = f[0];
-        S.fy[1][ty][tx] = f[1];
+        hi.Mv[0] = Mown[0]; hi.Mv[1] = Mown[1];
+        mu_face_t<MODE == MU_FULL>(kp, lo, hi, 1, fyo);
+        S.fy[0][ty][tx] = fyo[0];
+        S.fy[1][ty][tx] = fyo[1];
       }
       if (tid < TX + TY) {  // far faces: +y of the last row (warp 0), +x of the last column (warp 1)
         const int d = tid < TX ? 1 : 0;
@@ -327,38 +329,45 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
         else { S.fy[0][TY][c0 - 1] = f[0]; S.fy[1][TY][c0 - 1] = f[1]; }
       }
     }
-    double fzp[NMU], pn_c[NPH];
+    double fzp[NMU], pn_c[NPH], Mnx[NMU] = {0.0, 0.0};   // Mnx: own mobility at k+1
     if (fast_z && MODE == MU_NEIGHBOR) {
       fzp[0] = fzp[1] = 0.0;
 #pragma unroll
       for (int a = 0; a < NPH; ++a) pn_c[a] = T(S.pn[sn][a], orow, oc);
     } else if (fast_z) {
-      double Mn[NMU];
-      mob2(S.tab[slot(k + 1)], po_n, Mn);
+      mob2(S.tab[slot(k + 1)], po_n, Mnx);
 #pragma unroll
-      for (int c = 0; c < NMU; ++c)
-        fzp[c] = mu_flux_diff(kp, S.M[c][orow][oc], Mn[c], T(S.mu[s2][c], orow, oc), mu_n[c]);
+      for (int c = 0; c < NMU; ++c) fzp[c] = mu_flux_diff(kp, Mown[c], Mnx[c], mu_c[c], mu_n[c]);
 #pragma unroll
       for (int a = 0; a < NPH; ++a) pn_c[a] = T(S.pn[sn][a], orow, oc);
     } else {  // z-face k+1/2: own cell at k (shared memory) and at k+1 (registers;
               // the anti-trapping operands are only formed if the guards open)
       RawQ lo = rawq(k, oc, orow);
-      lo.Mv[0] = S.M[0][orow][oc]; lo.Mv[1] = S.M[1][orow][oc];
+      lo.Mv[0] = Mown[0]; lo.Mv[1] = Mown[1];
       const int s1 = slot(k + 1);
       ColQ hi{S, kp, s1, oc, orow, S.tab[s1], po_n, mu_n, {0.0, 0.0}};
       if (MODE == MU_FULL) mob2(S.tab[s1], po_n, hi.Mv);
       mu_face_t<MODE == MU_FULL>(kp, lo, hi, 2, fzp);
+      Mnx[0] = hi.Mv[0];
+      Mnx[1] = hi.Mv[1];
 #pragma unroll
       for (int a = 0; a < NPH; ++a) pn_c[a] = T(S.pn[sn][a], orow, oc);
+    }
+    // the divergence's own-face part before the barrier (the oracle's O5.9
+    // sum in another order: equal up to rounding)
+    double dpart[NMU];
+#pragma unroll
+    for (int c = 0; c < NMU; ++c) {
+      dpart[c] = ((fzp[c] - fzm[c]) - fxo[c]) - fyo[c];
+      fzm[c] = fzp[c];
+      Mown[c] = Mnx[c];
     }
     __syncthreads();  // E
     // F: cell update of (i, j, k)
     if (active) {
       double divf[NMU], out[NMU];
 #pragma unroll
-      for (int c = 0; c < NMU; ++c)
-        divf[c] = ((S.fx[c][ty][tx + 1] - S.fx[c][ty][tx]) + (S.fy[c][ty + 1][tx] - S.fy[c][ty][tx])) +
-                  (fzp[c] - fzm[c]);
+      for (int c = 0; c < NMU; ++c) divf[c] = dpart[c] + (S.fx[c][ty][tx + 1] + S.fy[c][ty + 1][tx]);
       const int64_t o = (int64_t)k * b.plane + colo;
       if (MODE != MU_NEIGHBOR) {
         mu_cell_update(kp, S.tab[sn], po_c, pn_c, mu_c, divf, out);
@@ -371,8 +380,6 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
         b.out[1][o] = out[1];
       }
     }
-    fzm[0] = fzp[0];
-    fzm[1] = fzp[1];
   }
 #undef T
 }
