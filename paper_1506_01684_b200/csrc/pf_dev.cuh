@@ -38,6 +38,7 @@ struct KParams {
   double omp[6];           // 16/pi^2 gamma_ab per pair
   double delta[6];         // cubic anisotropy per pair
   double g3[NPH];          // triple coefficient of the triple excluding x
+  double mch[NPH][NMU];    // m_a,c: the (T-independent) slope of c-hat, O5.5
   double pi_eps_4;         // pi eps / 4
   double Gv;               // G v = -dT/dt
   int aniso;
@@ -70,10 +71,9 @@ enum {
   T_KAPPA = 28,   // 2 A1 / (2A)^2
   T_MC = 36,      // D / (2A)
   T_B = 44,       // + a         L (T - T_eut) / T_eut
-  T_MCHAT = 48,   // m (as given; constant, kept for locality)
-  T_DI2A = 56,    // 1/(2A^l) - 1/(2A^a), solids a < 3
-  T_DCHAT = 62,   // chat^l - chat^a,     solids a < 3
-  TAB = 68        // multiple of 4 doubles (32 B): rows stay aligned
+  T_DI2A = 48,    // 1/(2A^l) - 1/(2A^a), solids a < 3
+  T_DCHAT = 54,   // chat^l - chat^a,     solids a < 3
+  TAB = 60        // multiple of 4 doubles (32 B): rows stay aligned
 };
 static_assert(TAB % 4 == 0, "table row alignment");
 // the (c = 0, 1) pair of phase a of a per-(phase, component) table entry
@@ -488,7 +488,7 @@ __device__ __forceinline__ void mu_cell_update(const KParams &kp, const double *
 #pragma unroll
   for (int a = 0; a < NPH; ++a) {
     const double2 i2a = tab2(tab, T_INV2A, a), ch = tab2(tab, T_CHAT, a);
-    const double2 mc = tab2(tab, T_MCHAT, a), ka = tab2(tab, T_KAPPA, a);
+    const double2 ka = tab2(tab, T_KAPPA, a);   // m_a,c: constant bank operand, no shared load
     const double e0 = mu[0] * i2a.x + ch.x, e1 = mu[1] * i2a.y + ch.y;
     X[0] += q[a] * i2a.x;
     X[1] += q[a] * i2a.y;
@@ -496,8 +496,8 @@ __device__ __forceinline__ void mu_cell_update(const KParams &kp, const double *
     A[1] += e1 * q[a];
     B[0] += e0 * p[a];
     B[1] += e1 * p[a];
-    D[0] += q[a] * (mc.x - mu[0] * ka.x);
-    D[1] += q[a] * (mc.y - mu[1] * ka.y);
+    D[0] += q[a] * (kp.mch[a][0] - mu[0] * ka.x);
+    D[1] += q[a] * (kp.mch[a][1] - mu[1] * ka.y);
   }
   const double P = So * Sn, Q = X[0] * X[1];
   const double R = 1.0 / (P * Q);

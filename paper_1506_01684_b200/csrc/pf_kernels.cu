@@ -35,7 +35,6 @@ __global__ void table_kernel(double *tab, int64_t nplanes, TabParams tp, int64_t
       row[T_CHAT + a * 2 + c] = tp.c0[a][c] + tp.m[a][c] * th;
       row[T_KAPPA + a * 2 + c] = 2.0 * tp.A1[a][c] * i2a * i2a;
       row[T_MC + a * 2 + c] = tp.D[a][c] * i2a;
-      row[T_MCHAT + a * 2 + c] = tp.m[a][c];
     }
   }
   for (int a = 0; a < 3; ++a)

@@ -886,6 +886,7 @@ pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
     for (int q = 0; q < 2; ++q) {
       tp.A0[a][q] = p->A0[a][q]; tp.A1[a][q] = p->A1[a][q]; tp.c0[a][q] = p->c0[a][q];
       tp.m[a][q] = p->m[a][q]; tp.D[a][q] = p->D[a][q];
+      kp.mch[a][q] = p->m[a][q];
     }
   }
   // decomposition
