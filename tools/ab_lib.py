@@ -14,4 +14,4 @@ with pfm.Context(n, n, n, prm, stream=s.cuda_stream) as ctx:
     ctx.init(cfg["seed"]); ctx.step(3); ctx.set_timing(True); ctx.step(20)
     inf = ctx.info()
     print(os.environ.get("PF_LIB", "default"), "v" + os.environ.get("VARIANT", "0"), "sc" + os.environ.get("SHORTCUTS", "0"), "aniso" if aniso else "iso", "phi", round(inf.ms_phi / inf.phi_launches, 3),
-          "mu", round(inf.ms_mu / inf.mu_launches, 3))
+          "mu", round(inf.ms_mu / inf.mu_launches, 3), "halo", round(inf.ms_halo / 20, 3))
