@@ -256,8 +256,10 @@ def run_gpu(args):
     ctx.set_timing(False)
     value = cells_local * world * args.steps / (ms / 1e3) / 1e6
 
-    # end-to-end through the C ABI with host buffers: each step writes the
-    # state from pinned host memory, advances one step, reads it back
+    # end-to-end through the C ABI with host buffers: each step uploads the
+    # state from pinned host memory, advances one step and reads it back —
+    # pf_step_io, which overlaps the upload, the sweeps and the download in
+    # z-slabs (= pf_write + pf_step(1) + pf_read, bit for bit)
     e2e = e2e_job = None
     state_bytes = cells_local * 6 * 8
     e2e_steps = min(args.steps, args.e2e_steps)
@@ -269,9 +271,7 @@ def run_gpu(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            ctx.write(hphi, hmu)
-            ctx.step(1)
-            ctx.read(hphi, hmu)
+            ctx.step_io(hphi, hmu, hphi, hmu)
         barrier()
         e2e_s = max_over_ranks(time.perf_counter() - t0)
         e2e = cells_local * world * e2e_steps / e2e_s / 1e6
@@ -346,7 +346,8 @@ def run_gpu(args):
             "e2e": {"value": round(e2e, 2) if e2e else None, "unit": "MLUP/s",
                     "h2d_bytes_per_step": state_bytes if e2e else 0,
                     "d2h_bytes_per_step": state_bytes if e2e else 0, "steps": e2e_steps,
-                    "what": "pf_write(pinned host state) + pf_step(1) + pf_read(pinned host) per step",
+                    "what": "pf_step_io(pinned host state in, pinned host state out) per step: upload, step and download "
+                            "overlapped in z-slabs (single block per GPU; else pf_write + pf_step(1) + pf_read)",
                     "job": {"value": round(e2e_job, 2) if e2e_job else None, "steps": args.steps,
                             "what": "pf_write(pinned host state) once + pf_step(steps) + pf_read(pinned host) once"}},
             "gpu_launches": launches,

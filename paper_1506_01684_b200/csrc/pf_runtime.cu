@@ -115,6 +115,17 @@ struct pf_ctx {
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};
   int64_t graph_launches[2] = {0, 0};
   int64_t *d_step = nullptr;       // device copy of the time level for the table kernel
+  // pf_step_io on a single-block context: the block cut into z-slabs, ghost
+  // copy lists per slab (both fields, both copies), per-slab events, the
+  // upload and download streams
+  struct SlabIO {
+    int H = 0, S = 0;                      // slab height, slab count
+    std::vector<CopyOp *> ops[2][2];       // [field][copy][slab]
+    std::vector<int> nops[2][2];
+    std::vector<int64_t> nctas[2][2];
+    std::vector<cudaEvent_t> ev_up, ev_mu;
+    cudaStream_t up = nullptr, dn = nullptr;
+  } sio;
 };
 
 namespace {
@@ -585,6 +596,116 @@ pf_status nan_check(pf_ctx *c) {
                   (long long)(b.y0 + j), (long long)(b.z0 + k));
     }
   }
+  return PF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// pf_step_io: one step from a host state to a host state on a single-block
+// context, cut into z-slabs so that the upload of slab s+1, the sweeps of the
+// slabs before it and the download of finished slabs overlap (PCIe is full
+// duplex; the step's compute is a few percent of its transfer time).  Every
+// kernel is the one pf_step launches, on a view shifted to the slab's planes;
+// chunk edges do not change a face's bits (pinned rounding), so the result is
+// pf_write + pf_step(1) + pf_read bit for bit.
+// ---------------------------------------------------------------------------
+BlockView slab_view(BlockView v, int field_out, int z0, int z1) {
+  const int64_t o = (int64_t)z0 * v.plane;
+  for (int a = 0; a < NPH; ++a) { v.phi[a] += o; v.phin[a] += o; }
+  for (int q = 0; q < NMU; ++q) v.mu[q] += o;
+  for (int a = 0; a < (field_out == 0 ? NPH : NMU); ++a) v.out[a] += o;
+  v.nz = z1 - z0;
+  v.zoff += z0;
+  v.tab += (int64_t)z0 * TAB;
+  return v;
+}
+
+// ghost copies of one field / copy restricted to planes [z0, z1) of the single
+// block: the 26 directions, the wall planes only with the first / last slab
+pf_status slab_ops(pf_ctx *c, int field, int copy, int z0, int z1, CopyOp **d, int *nops, int64_t *nctas) {
+  const Block &B = c->blocks[0];
+  const int ncomp = field == 0 ? NPH : NMU;
+  std::vector<CopyOp> ops;
+  for (const auto &dir : ghost_dirs()) {
+    Region r = ghost_region(c, B.bx, B.by, B.bz, dir, B.nx, B.ny, B.nz);
+    if (dir[2] == 0) { r.ds[2] = r.ss[2] = z0; r.ext[2] = z1 - z0; }
+    else if ((dir[2] < 0 && z0 != 0) || (dir[2] > 0 && z1 != B.nz)) continue;
+    CopyOp op{};
+    for (int cc = 0; cc < ncomp; ++cc) {
+      op.src[cc] = field_ptr(B, field, copy, cc) + cell_off(B, r.ss[0], r.ss[1], r.ss[2]);
+      op.dst[cc] = field_ptr(B, field, copy, cc) + cell_off(B, r.ds[0], r.ds[1], r.ds[2]);
+    }
+    op.ssx = op.dsx = 1; op.ssy = op.dsy = B.pitch; op.ssz = op.dsz = B.plane;
+    op.ex = (int)r.ext[0]; op.ey = (int)r.ext[1]; op.ez = (int)r.ext[2]; op.ncomp = ncomp;
+    op.xpad = ghost_xpad(r, B.nx);
+    ops.push_back(op);
+  }
+  *nops = (int)ops.size();
+  *d = nullptr;
+  return upload_ops(c, ops, d, nctas);
+}
+
+pf_status slab_setup(pf_ctx *c) {
+  auto &io = c->sio;
+  if (io.S) return PF_OK;
+  const int nz = c->blocks[0].nz;
+#ifndef PF_SLABS
+#define PF_SLABS 32   // measured at 512^3: 16 -> 151.9, 32 -> 147.3, 64 -> 150.7 ms per step
+#endif
+  // ~PF_SLABS slabs: the download of slab s waits for the upload of slab s+2,
+  // so the pipeline's fill + drain cost ~4 slabs of one-way transfer time
+  io.H = std::max(4, (nz + PF_SLABS - 1) / PF_SLABS);
+  io.S = (nz + io.H - 1) / io.H;
+  CK(cudaStreamCreateWithFlags(&io.up, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&io.dn, cudaStreamNonBlocking));
+  io.ev_up.assign(io.S, nullptr);
+  io.ev_mu.assign(io.S, nullptr);
+  for (int s = 0; s < io.S; ++s) {
+    CK(cudaEventCreateWithFlags(&io.ev_up[s], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&io.ev_mu[s], cudaEventDisableTiming));
+  }
+  for (int f = 0; f < 2; ++f)
+    for (int cp = 0; cp < 2; ++cp) {
+      io.ops[f][cp].assign(io.S, nullptr);
+      io.nops[f][cp].assign(io.S, 0);
+      io.nctas[f][cp].assign(io.S, 0);
+      for (int s = 0; s < io.S; ++s)
+        CKS(slab_ops(c, f, cp, s * io.H, std::min(nz, (s + 1) * io.H), &io.ops[f][cp][s], &io.nops[f][cp][s],
+                     &io.nctas[f][cp][s]));
+    }
+  return PF_OK;
+}
+
+void slab_free(pf_ctx *c) {
+  auto &io = c->sio;
+  for (int f = 0; f < 2; ++f)
+    for (int cp = 0; cp < 2; ++cp)
+      for (auto *p : io.ops[f][cp]) if (p) cudaFree(p);
+  for (auto e : io.ev_up) if (e) cudaEventDestroy(e);
+  for (auto e : io.ev_mu) if (e) cudaEventDestroy(e);
+  if (io.up) { cudaStreamSynchronize(io.up); cudaStreamDestroy(io.up); }
+  if (io.dn) { cudaStreamSynchronize(io.dn); cudaStreamDestroy(io.dn); }
+  io = pf_ctx::SlabIO{};
+}
+
+// interior planes [z0, z1) of copy `copy` <-> the compact host state (DMA
+// straight into / out of the padded layout: one 3D copy per component)
+pf_status slab_copy(pf_ctx *c, int copy, const double *phi, const double *mu, int z0, int z1, bool up,
+                    cudaStream_t st) {
+  const Block &b = c->blocks[0];
+  const int64_t n = (int64_t)b.nx * b.ny * b.nz;
+  for (int field = 0; field < 2; ++field)
+    for (int q = 0; q < (field == 0 ? NPH : NMU); ++q) {
+      double *h = const_cast<double *>(field == 0 ? phi : mu) + q * n;
+      double *dv = field_ptr(b, field, copy, q);
+      cudaPitchedPtr hp = make_cudaPitchedPtr(h, (size_t)b.nx * 8, (size_t)b.nx * 8, (size_t)b.ny);
+      cudaPitchedPtr dp = make_cudaPitchedPtr(dv, (size_t)b.pitch * 8, (size_t)b.pitch * 8, (size_t)b.ny + 2);
+      const cudaPos hpos = make_cudaPos(0, 0, (size_t)z0), dpos = make_cudaPos(XO * 8, 1, (size_t)(z0 + 1 + b.woff));
+      cudaMemcpy3DParms m = {};
+      if (up) { m.srcPtr = hp; m.srcPos = hpos; m.dstPtr = dp; m.dstPos = dpos; m.kind = cudaMemcpyHostToDevice; }
+      else { m.srcPtr = dp; m.srcPos = dpos; m.dstPtr = hp; m.dstPos = hpos; m.kind = cudaMemcpyDeviceToHost; }
+      m.extent = make_cudaExtent((size_t)b.nx * 8, (size_t)b.ny, (size_t)(z1 - z0));
+      CK(cudaMemcpy3DAsync(&m, st));
+    }
   return PF_OK;
 }
 
@@ -1176,6 +1297,70 @@ pf_status pf_step(pf_ctx *c, int64_t n) {
   return PF_OK;
 }
 
+pf_status pf_step_io(pf_ctx *c, const double *phi_in, const double *mu_in, double *phi_out, double *mu_out) {
+  CKS(check_state(c, false));
+  if (!phi_in || !mu_in || !phi_out || !mu_out) return fail(c, PF_ERR_ARG, "NULL state pointer");
+  const bool host = !is_device_ptr(phi_in) && !is_device_ptr(mu_in) && !is_device_ptr(phi_out) &&
+                    !is_device_ptr(mu_out);
+  // the slab pipeline covers one block per process, no window, the tiled
+  // sweeps and the Algorithm-1 mu update (overlap 0 / 1 are bitwise equal);
+  // anything else is the same sequence of calls without the overlap
+  if (!host || c->g.nranks != 1 || c->blocks.size() != 1 || c->p.window || c->p.variant == 1 ||
+      (c->p.overlap != 0 && c->p.overlap != 1)) {
+    CKS(pf_write(c, phi_in, mu_in));
+    CKS(pf_step(c, 1));
+    return pf_read(c, phi_out, mu_out);
+  }
+  CKS(join_mu(c));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaStreamSynchronize(c->cstream));
+  CKS(slab_setup(c));
+  auto &io = c->sio;
+  Block &b = c->blocks[0];
+  const int src = c->cur, dst = c->cur ^ 1, S = io.S;
+  auto zs = [&](int s) { return std::min(b.nz, s * io.H); };
+  for (int s = 0; s < S; ++s) {   // every upload back to back
+    CKS(slab_copy(c, src, phi_in, mu_in, zs(s), zs(s + 1), true, io.up));
+    CK(cudaEventRecord(io.ev_up[s], io.up));
+  }
+  launch_table(c->stream, c->d_tab, c->tab_planes, c->tp, c->step, c->zorig, nullptr);
+  c->launches++;
+  // iteration s: ghosts of input slab s; phi-sweep of slab s-1 (needs plane
+  // z_s of the input) + its phi^{n+1} ghosts; mu-sweep of slab s-2 (needs
+  // phi^{n+1} up to plane z_{s-1}) + the download of slab s-2
+  for (int s = 0; s <= S + 1; ++s) {
+    if (s < S) {
+      CK(cudaStreamWaitEvent(c->stream, io.ev_up[s], 0));
+      for (int f = 0; f < 2; ++f) {
+        launch_copy(c->stream, io.ops[f][src][s], io.nops[f][src][s], io.nctas[f][src][s]);
+        c->launches++;
+      }
+    }
+    if (s >= 1 && s <= S) {
+      launch_phi_tiled(c->stream, c->kp, slab_view(view(c, b, 0), 0, zs(s - 1), zs(s)), maps_of(c, b, 0));
+      launch_copy(c->stream, io.ops[0][dst][s - 1], io.nops[0][dst][s - 1], io.nctas[0][dst][s - 1]);
+      c->launches += 2;
+    }
+    if (s >= 2) {
+      launch_mu_tiled(c->stream, c->kp, slab_view(view(c, b, 1), 1, zs(s - 2), zs(s - 1)), maps_of(c, b, 1), MU_FULL);
+      c->launches++;
+      CK(cudaEventRecord(io.ev_mu[s - 2], c->stream));
+      CK(cudaStreamWaitEvent(io.dn, io.ev_mu[s - 2], 0));
+      CKS(slab_copy(c, dst, phi_out, mu_out, zs(s - 2), zs(s - 1), false, io.dn));
+    }
+    CK(cudaGetLastError());
+  }
+  CKS(exchange(c, 1, dst));   // mu^{n+1} ghosts: the device keeps a complete time level
+  CK(cudaStreamSynchronize(io.dn));
+  CK(cudaStreamSynchronize(c->stream));
+  c->cur ^= 1;
+  c->step += 1;
+  c->initialized = true;
+  c->next_check = c->step;
+  if (c->p.nan_check_every > 0 && c->step % c->p.nan_check_every == 0) CKS(nan_check(c));
+  return PF_OK;
+}
+
 pf_status pf_read(pf_ctx *c, double *phi, double *mu) {
   CKS(check_state(c, true));
   if (!phi || !mu) return fail(c, PF_ERR_ARG, "NULL state pointer");
@@ -1410,6 +1595,7 @@ void pf_destroy(pf_ctx *c) {
     if (c->d_send[f]) cudaFree(c->d_send[f]);
     if (c->d_recv[f]) cudaFree(c->d_recv[f]);
   }
+  slab_free(c);
   if (c->d_tab) cudaFree(c->d_tab);
   if (c->d_red) cudaFree(c->d_red);
   if (c->d_step) cudaFree(c->d_step);

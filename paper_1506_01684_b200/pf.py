@@ -28,7 +28,7 @@ PF_OK, PF_ERR_CONFIG, PF_ERR_NUMERICAL, PF_ERR_CUDA, PF_ERR_COMM, PF_ERR_STATE, 
 STATUS_NAMES = {0: "PF_OK", -1: "PF_ERR_CONFIG", -2: "PF_ERR_NUMERICAL", -3: "PF_ERR_CUDA", -4: "PF_ERR_COMM",
                 -5: "PF_ERR_STATE", -6: "PF_ERR_ARG", -7: "PF_ERR_IO"}
 EXPORTS = ["pf_nccl_unique_id", "pf_halo_plan", "pf_create", "pf_init", "pf_write", "pf_set_time", "pf_step", "pf_read",
-           "pf_save", "pf_load", "pf_mesh", "pf_mesh_table", "pf_set_timing", "pf_info", "pf_last_error", "pf_destroy"]
+           "pf_step_io", "pf_save", "pf_load", "pf_mesh", "pf_mesh_table", "pf_set_timing", "pf_info", "pf_last_error", "pf_destroy"]
 
 
 def mesh_table():
@@ -91,6 +91,7 @@ def lib():
         L.pf_set_time.argtypes = [vp, I64, I64]
         L.pf_step.argtypes = [vp, I64]
         L.pf_read.argtypes = [vp, vp, vp]
+        L.pf_step_io.argtypes = [vp, vp, vp, vp, vp]
         L.pf_save.argtypes = [vp, ctypes.c_char_p]
         L.pf_load.argtypes = [vp, ctypes.c_char_p]
         L.pf_mesh.argtypes = [vp, I32, D, I64, vp, vp, ctypes.POINTER(I64)]
@@ -230,6 +231,15 @@ class Context:
             mu = np.empty((2,) + self.shape)
         self._check(lib().pf_read(self._c, _ptr(phi), _ptr(mu)))
         return phi, mu
+
+    def step_io(self, phi_in, mu_in, phi_out=None, mu_out=None):
+        """One step from a host state to a host state (pf_step_io: upload, sweeps and
+        download overlapped in z-slabs; = write + step(1) + read, bit for bit)."""
+        if phi_out is None:
+            phi_out = np.empty((4,) + self.shape)
+            mu_out = np.empty((2,) + self.shape)
+        self._check(lib().pf_step_io(self._c, _ptr(phi_in), _ptr(mu_in), _ptr(phi_out), _ptr(mu_out)))
+        return phi_out, mu_out
 
     def save(self, path):
         """FP32 checkpoint of the current state (pf_save; collective)."""
