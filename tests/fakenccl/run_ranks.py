@@ -69,8 +69,12 @@ def rank_main(r):
             lphi, lmu = c.read()
             res = {"resumed_equal_cast": True, "lphi": lphi, "lmu": lmu}
         else:
-            c.step(steps)
-            gphi, gmu = c.read()
+            if spec.get("step_io"):    # the last step through pf_step_io (collective; multi-rank: the plain calls)
+                c.step(steps - 1)
+                gphi, gmu = c.step_io(*c.read())
+            else:
+                c.step(steps)
+                gphi, gmu = c.read()
             mesh = [c.mesh(a) for a in range(4)] if spec.get("mesh") else None
             res = {}
         res.update(box=(x0, y0, z0, nx, ny, nz), phi=gphi, mu=gmu, shifts=int(c.info().shifts))

@@ -48,6 +48,11 @@ def test_ranks_overlap_modes(fakelib, overlap):
     assert out["equal_phi"] and out["equal_mu"]
 
 
+def test_ranks_step_io(fakelib):
+    out = _run(fakelib, grid=[32, 24, 20], blocks=[2, 1, 2], steps=6, step_io=True, layer_height=9.5)
+    assert out["equal_phi"] and out["equal_mu"]
+
+
 def test_ranks_window_aniso(fakelib):
     # forced window shifts through the allreduce(max) of the front, D3C19 halos
     out = _run(fakelib, grid=[24, 24, 24], blocks=[2, 2, 2], steps=30, window=True, config="c5",
