@@ -45,6 +45,19 @@ struct KParams {
   int shortcuts;           // region shortcuts (NEXT-1): skip the phi update of bulk warps
 };
 
+// 1/s to within an ulp (faithful, not correctly rounded): the hardware
+// approximation refined by two Newton steps (each doubles the correct bits),
+// without the IEEE division's special-case branch.  For s > 0 normal; exact
+// where 1/s is a power of two (s = 1 gives 1).
+__device__ __forceinline__ double rcp_nr(double s) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
+  double e = __fma_rn(-s, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-s, r, 1.0);
+  return __fma_rn(r, e, r);
+}
+
 // A cell whose phase vector is a simplex vertex (one component exactly 1, the
 // others exactly 0).  With an identical neighbourhood its phi update returns
 // it unchanged bit for bit: every gradient and face flux is exactly 0, the
@@ -283,7 +296,7 @@ __device__ __forceinline__ void phi_cell_rhs0(const KParams &kp, const double *_
     ps[a] = s;
   }
   const double S = ph[0] * ph[0] + ph[1] * ph[1] + ph[2] * ph[2] + ph[3] * ph[3];
-  const double rS = 1.0 / S;
+  const double rS = 1.0 / S;   // (rcp_nr here measured +0.7 %: the FP64 pipe, not latency, binds)
   const double pbar = rS * (ph[0] * ph[0] * ps[0] + ph[1] * ph[1] * ps[1] + ph[2] * ph[2] * ps[2] +
                             ph[3] * ph[3] * ps[3]);
   const double epsT = tab[T_EPST], Teps = tab[T_TEPS];
@@ -507,7 +520,10 @@ __device__ __forceinline__ void mu_cell_update(const KParams &kp, const double *
     D[1] += q[a] * (kp.mch[a][1] - mu[1] * ka.y);
   }
   const double P = So * Sn, Q = X[0] * X[1];
-  const double R = 1.0 / (P * Q);
+  // faithful reciprocal: the latency-bound mu-sweep gains from the shorter
+  // chain (measured -2 %); P Q is a product of O(1) sums, far from the
+  // subnormal range rcp.approx.ftz would flush
+  const double R = rcp_nr(P * Q);
   const double QR = Q * R, PR = P * R;
   const double rSn = So * QR, rSo = Sn * QR;           // 1/Sn, 1/So
   const double dtSn = kp.dt * Sn;
