@@ -123,6 +123,9 @@ struct pf_ctx {
     std::vector<CopyOp *> ops[2][2];       // [field][copy][slab]
     std::vector<int> nops[2][2];
     std::vector<int64_t> nctas[2][2];
+    std::vector<CopyOp *> ops_x[2];        // phi^{n+1} ghosts of slab s + the next slab's first plane, [copy][slab]
+    std::vector<int> nops_x[2];
+    std::vector<int64_t> nctas_x[2];
     std::vector<cudaEvent_t> ev_up, ev_mu;
     cudaStream_t up = nullptr, dn = nullptr;
   } sio;
@@ -672,6 +675,14 @@ pf_status slab_setup(pf_ctx *c) {
         CKS(slab_ops(c, f, cp, s * io.H, std::min(nz, (s + 1) * io.H), &io.ops[f][cp][s], &io.nops[f][cp][s],
                      &io.nctas[f][cp][s]));
     }
+  for (int cp = 0; cp < 2; ++cp) {
+    io.ops_x[cp].assign(io.S, nullptr);
+    io.nops_x[cp].assign(io.S, 0);
+    io.nctas_x[cp].assign(io.S, 0);
+    for (int s = 0; s < io.S; ++s)
+      CKS(slab_ops(c, 0, cp, s * io.H, std::min(nz, (s + 1) * io.H + 1), &io.ops_x[cp][s], &io.nops_x[cp][s],
+                   &io.nctas_x[cp][s]));
+  }
   return PF_OK;
 }
 
@@ -680,6 +691,8 @@ void slab_free(pf_ctx *c) {
   for (int f = 0; f < 2; ++f)
     for (int cp = 0; cp < 2; ++cp)
       for (auto *p : io.ops[f][cp]) if (p) cudaFree(p);
+  for (int cp = 0; cp < 2; ++cp)
+    for (auto *p : io.ops_x[cp]) if (p) cudaFree(p);
   for (auto e : io.ev_up) if (e) cudaEventDestroy(e);
   for (auto e : io.ev_mu) if (e) cudaEventDestroy(e);
   if (io.up) { cudaStreamSynchronize(io.up); cudaStreamDestroy(io.up); }
@@ -1325,10 +1338,12 @@ pf_status pf_step_io(pf_ctx *c, const double *phi_in, const double *mu_in, doubl
   }
   launch_table(c->stream, c->d_tab, c->tab_planes, c->tp, c->step, c->zorig, nullptr);
   c->launches++;
-  // iteration s: ghosts of input slab s; phi-sweep of slab s-1 (needs plane
-  // z_s of the input) + its phi^{n+1} ghosts; mu-sweep of slab s-2 (needs
-  // phi^{n+1} up to plane z_{s-1}) + the download of slab s-2
-  for (int s = 0; s <= S + 1; ++s) {
+  // iteration s: ghosts of input slab s; then slab s-1: its phi-sweep, extended
+  // by the first plane of slab s (needs input planes up to z_s + 1, in slab s)
+  // so that its mu-sweep (phi^{n+1} up to plane z_s) and its download follow at
+  // once — the download of slab s-1 waits for the upload of slab s only.  The
+  // extra plane is computed again, to the same bits, by the next slab's sweep.
+  for (int s = 0; s <= S; ++s) {
     if (s < S) {
       CK(cudaStreamWaitEvent(c->stream, io.ev_up[s], 0));
       for (int f = 0; f < 2; ++f) {
@@ -1336,17 +1351,15 @@ pf_status pf_step_io(pf_ctx *c, const double *phi_in, const double *mu_in, doubl
         c->launches++;
       }
     }
-    if (s >= 1 && s <= S) {
-      launch_phi_tiled(c->stream, c->kp, slab_view(view(c, b, 0), 0, zs(s - 1), zs(s)), maps_of(c, b, 0));
-      launch_copy(c->stream, io.ops[0][dst][s - 1], io.nops[0][dst][s - 1], io.nctas[0][dst][s - 1]);
-      c->launches += 2;
-    }
-    if (s >= 2) {
-      launch_mu_tiled(c->stream, c->kp, slab_view(view(c, b, 1), 1, zs(s - 2), zs(s - 1)), maps_of(c, b, 1), MU_FULL);
-      c->launches++;
-      CK(cudaEventRecord(io.ev_mu[s - 2], c->stream));
-      CK(cudaStreamWaitEvent(io.dn, io.ev_mu[s - 2], 0));
-      CKS(slab_copy(c, dst, phi_out, mu_out, zs(s - 2), zs(s - 1), false, io.dn));
+    if (s >= 1) {
+      const int z0 = zs(s - 1), z1 = zs(s), z1x = std::min(b.nz, z1 + 1);
+      launch_phi_tiled(c->stream, c->kp, slab_view(view(c, b, 0), 0, z0, z1x), maps_of(c, b, 0));
+      launch_copy(c->stream, io.ops_x[dst][s - 1], io.nops_x[dst][s - 1], io.nctas_x[dst][s - 1]);
+      launch_mu_tiled(c->stream, c->kp, slab_view(view(c, b, 1), 1, z0, z1), maps_of(c, b, 1), MU_FULL);
+      c->launches += 3;
+      CK(cudaEventRecord(io.ev_mu[s - 1], c->stream));
+      CK(cudaStreamWaitEvent(io.dn, io.ev_mu[s - 1], 0));
+      CKS(slab_copy(c, dst, phi_out, mu_out, z0, z1, false, io.dn));
     }
     CK(cudaGetLastError());
   }
