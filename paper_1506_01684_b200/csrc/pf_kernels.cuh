@@ -30,12 +30,11 @@ constexpr int PHI_TILE_X = PF_PHI_TX, PHI_TILE_Y = PF_PHI_TY, MU_TILE_X = PF_MU_
 
 // TMA descriptors of one block's fields in one time level (encoded on the host
 // over the whole padded allocation: dims {pitch, ny+2, planes}, x fastest).
-// tile: box (TX+2) x (TY+2) x 1 — interior tile + ring; int: box TX x TY x 1.
+// tile: box (TX+4) x (TY+2) x 1 — interior tile + ring, x from a 16-byte boundary.
 struct TmaMaps {
   CUtensorMap phi[NPH];   // phi^n,     tile box
   CUtensorMap phin[NPH];  // phi^{n+1}, tile box
   CUtensorMap mu[NMU];    // mu^n,      tile box
-  CUtensorMap mui[NMU];   // mu^n,      interior box
 };
 
 // Pointers into one block's fields, offset to interior cell (0,0,0) of the

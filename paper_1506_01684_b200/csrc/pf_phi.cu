@@ -1,17 +1,18 @@
 // pf_phi.cu — production phi-sweep (Eq. (1)-(2)): z-marching
 // 2.5D tiles with every staggered face flux (PAPER.md:299-317,
 // fig:staggeredBuffer) evaluated exactly once:
-//   * x- and y-faces of plane k: each thread evaluates its -x and -y face, warps
-//     0/1 the tile's far +y / +x faces; results go to shared memory and are read
-//     by both adjacent cells;
+//   * x- and y-faces of plane k: each thread evaluates its -x and -y face, warp
+//     0 the tile's far +y / +x faces; results go to shared memory (buffers
+//     alternating with the plane's parity) and are read by both adjacent cells;
 //   * z-faces: carried in registers from k-1/2 to k+1/2 (the paper's Nx x Ny
-//     staggered buffer becomes one register set per column).
+//     staggered buffer becomes one register set per column; anisotropic: a
+//     thread-private shared-memory slot).
 // Data movement: per plane, one elected thread issues TMA bulk-tensor copies of
-// the 4 phi tiles (interior + ring, (TX+2) x (TY+2) boxes), the 2 mu interior
-// boxes and a bulk copy of the table row, two planes ahead, into 4 rotating
-// slots guarded by mbarriers.  Two CTA barriers per plane.  The face and
-// gradient routines are the pinned ones of pf_dev.cuh: a face evaluated at a
-// tile / chunk / block edge has the same bits as mid-tile.
+// the 4 phi tiles (interior + ring + corners) and a bulk copy of the table row,
+// two planes ahead, into 4 rotating slots guarded by mbarriers; mu (the cell's
+// own value only) comes from global memory one plane ahead.  One CTA barrier
+// per plane.  The face and gradient routines are the pinned ones of pf_dev.cuh:
+// a face evaluated at a tile / chunk / block edge has the same bits as mid-tile.
 #include "pf_kernels.cuh"
 #define PF_TILE_X PHI_TILE_X
 #define PF_TILE_Y PHI_TILE_Y

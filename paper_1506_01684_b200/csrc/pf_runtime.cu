@@ -43,8 +43,7 @@ struct Block {
   int woff;                  // window offset (planes)
   CUtensorMap tphi[2][NPH];  // TMA maps per time level: phi tile box (phi-sweep tile),
   CUtensorMap tphim[2][NPH]; //   phi tile box (mu-sweep tile),
-  CUtensorMap tmu[2][NMU];   //   mu tile box (mu-sweep tile),
-  CUtensorMap tmui[2][NMU];  //   mu interior box (phi-sweep tile)
+  CUtensorMap tmu[2][NMU];   //   mu tile box (mu-sweep tile)
 };
 
 struct Plan {                // halo plan of one field in one copy
@@ -287,7 +286,6 @@ pf_status encode_maps(pf_ctx *c, Block &b) {
     }
     for (int q = 0; q < NMU; ++q) {
       CKS(encode_map(c, &b.tmu[cp][q], b.mu[cp][q], b, MU_TILE_X + 4, MU_TILE_Y + 2));
-      CKS(encode_map(c, &b.tmui[cp][q], b.mu[cp][q], b, PHI_TILE_X, PHI_TILE_Y));
     }
   }
   return PF_OK;
@@ -302,7 +300,7 @@ TmaMaps maps_of(const pf_ctx *c, const Block &b, int field) {
     t.phi[a] = field == 0 ? b.tphi[s][a] : b.tphim[s][a];
     t.phin[a] = b.tphim[d][a];
   }
-  for (int q = 0; q < NMU; ++q) { t.mu[q] = b.tmu[s][q]; t.mui[q] = b.tmui[s][q]; }
+  for (int q = 0; q < NMU; ++q) t.mu[q] = b.tmu[s][q];
   return t;
 }
 
