@@ -6,8 +6,8 @@
 // z only; the per-plane table row is staged once per plane).  A tile plane in
 // shared memory is (TX+2) x (TY+2) cells: the interior plus a one-cell ring
 // (with the 4 in-plane corners, needed by the D3C19 tangential gradients).
-// Planes are staged two ahead with cp.async (LDGSTS: global -> shared without
-// registers), so the loads of plane k+2 overlap the compute of plane k.
+// Planes are staged ahead by TMA bulk-tensor copies (below), so the loads of
+// plane k+2 overlap the compute of plane k.
 #pragma once
 #include <algorithm>
 #include <cmath>
@@ -37,15 +37,6 @@ __device__ __forceinline__ void ring_cell(int r, int &col, int &row) {
 __device__ __forceinline__ bool ring_corner(int col, int row) {
   return (col == 0 || col == RX - 1) && (row == 0 || row == RY - 1);
 }
-
-// 8-byte async copy global -> shared; !ok zero-fills (src-size 0)
-__device__ __forceinline__ void cp_async8(void *smem, const double *gmem, bool ok) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(ok ? 8 : 0) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // ---------------------------------------------------------------------------
 // TMA (cp.async.bulk.tensor) + mbarrier helpers.  One elected thread arms the
