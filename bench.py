@@ -234,6 +234,10 @@ def run_gpu(args):
     # beside the next phi-sweep)
     clocks = ClockSampler(local if world > 1 else 0)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # per-sweep device times for the roofline, live inside the timed region:
+    # CUDA events around each sweep on the launching stream (pf_set_timing;
+    # a graph replay has no per-sweep events, so --graph times them after)
+    ctx.set_timing(not args.graph)
     l0 = ctx.info().launches
     barrier()
     torch.cuda.synchronize()
@@ -246,10 +250,9 @@ def run_gpu(args):
     clk = clocks.stop()
     ms = max_over_ranks(e0.elapsed_time(e1))
     launches = int(ctx.info().launches - l0)
-    # per-sweep device times for the roofline: the same kernels launched one by
-    # one with CUDA events around each on the launching stream (pf_set_timing)
-    ctx.set_timing(True)
-    ctx.step(min(args.steps, 10))
+    if args.graph:
+        ctx.set_timing(True)
+        ctx.step(min(args.steps, 10))
     inf = ctx.info()
     ms_phi = inf.ms_phi / max(1, inf.phi_launches)
     ms_mu = inf.ms_mu / max(1, inf.mu_launches)
