@@ -149,12 +149,15 @@ __device__ __forceinline__ double pair_grad_aniso_d(double g2, double delta, con
 // (oracle O4.5): phibar = (lo+hi)/2, normal gradient (hi-lo)/dx, tangential
 // gradient = mean of the two centre gradients (anisotropic only);
 // j_a = -sum_{b != a} g_ab,d(q_ab) phibar_b.  Pinned rounding.
+// AN: -1 = the model from kp.aniso at run time, 0 / 1 = isotropic / anisotropic
+// fixed at compile time (the tiled sweep's two kernels carry only their own code)
+template <int AN = -1>
 __device__ __forceinline__ void phi_face(const KParams &kp, const double plo[NPH], const double phi_[NPH],
                                          const double glo[NPH][3], const double ghi[NPH][3], int d,
                                          double jf[NPH]) {
 #pragma unroll
   for (int a = 0; a < NPH; ++a) jf[a] = 0.0;
-  if (!kp.aniso) {
+  if (!(AN < 0 ? kp.aniso != 0 : AN == 1)) {
     // isotropic: with s = lo + hi = 2 phibar and t = hi - lo = dx grad_d phi,
     // j_a = -sum_b 2 gamma_ab (phibar_a grad_b - phibar_b grad_a) phibar_b
     //     = -sum_b [2 gamma_ab / (4 dx)] (s_a t_b - s_b t_a) s_b,
@@ -212,6 +215,7 @@ __device__ __forceinline__ double cgrad(const KParams &kp, double lo, double hi)
 // face fluxes before its CTA barrier: phi_cell_rhs0 returns
 // r0_a = eps T da/dphi_a + (T/eps) domega/dphi_a + dpsi/dphi_a (O4.2-4.4,
 // 4.7-4.8), phi_cell_finish adds the divergence and does O4.9-4.11.
+template <int AN = -1>
 __device__ __forceinline__ void phi_cell_rhs0(const KParams &kp, const double *__restrict__ tab,
                                               const double ph[NPH], const double mu[NMU],
                                               const double gc[NPH][3], double r0[NPH]);
@@ -239,12 +243,13 @@ __device__ __forceinline__ void phi_cell_update(const KParams &kp, const double 
   phi_cell_update_div(kp, tab, ph, mu, gc, dsum, out);
 }
 
+template <int AN>
 __device__ __forceinline__ void phi_cell_rhs0(const KParams &kp, const double *__restrict__ tab,
                                               const double ph[NPH], const double mu[NMU],
                                               const double gc[NPH][3], double r0[NPH]) {
   // d a / d phi_a = sum_{b != a} g_ab(q_ab) . grad phi_b   (O4.2-4)
   double dad[NPH] = {0.0, 0.0, 0.0, 0.0};
-  if (!kp.aniso) {
+  if (!(AN < 0 ? kp.aniso != 0 : AN == 1)) {
     // isotropic g = 2 gamma q: q_ab . grad_b = phi_a |grad_b|^2 - phi_b (grad_a . grad_b),
     // so dad_a = sum_b 2 gamma_ab (phi_a G_bb - phi_b G_ab) with the Gram matrix G
     // of the centre differences (g2mc carries 2 gamma / (2 dx)^2)

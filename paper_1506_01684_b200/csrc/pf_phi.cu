@@ -48,6 +48,10 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
   const int64_t colo = (int64_t)j * b.pitch + i;
   const int oc = tx + 1, orow = ty + 1;            // own tile coordinates
 #define T(arr, row, col) TILE_AT(arr, row, col)
+// the face and cell routines specialised for this kernel's model: each of the
+// two kernels carries only its own code (measured: iso -1.8 %, aniso -6 %;
+// 35 % less code, fewer instruction-fetch stalls)
+#define PF_AN (ANISO ? 1 : 0)
 
   auto slot = [&](int k) { return (k - k0 + 1) & (NSLOT - 1); };
   auto parity = [&](int k) { return (uint32_t)(((k - k0 + 1) >> 2) & 1); };
@@ -103,7 +107,7 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
       tan_grad(s0, s0, s0, oc, orow, 2, gl);
       tan_grad(s1, s1, s1, oc, orow, 2, gh);
     }
-    phi_face(kp, lo, hi, ANISO ? gl : gdum, ANISO ? gh : gdum, 2, jzm);
+    phi_face<PF_AN>(kp, lo, hi, ANISO ? gl : gdum, ANISO ? gh : gdum, 2, jzm);
     if (ANISO)
 #pragma unroll
       for (int a = 0; a < NPH; ++a) S.jz[a][ty][tx] = jzm[a];
@@ -157,7 +161,7 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
           hi[a] = ANISO ? T(S.p[sc][a], orow, oc) : pc[a];   // anisotropic: re-read (registers)
         }
         if (ANISO) tan_grad(sc, sm, sp, lc, lr, d, gl);
-        phi_face(kp, lo, hi, ANISO ? gl : gdum, ANISO ? gown : gdum, d, jf);
+        phi_face<PF_AN>(kp, lo, hi, ANISO ? gl : gdum, ANISO ? gown : gdum, d, jf);
 #pragma unroll
         for (int a = 0; a < NPH; ++a) {
           if (d == 0) S.fx[fb][a][ty][tx] = jf[a];
@@ -176,7 +180,7 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
           tan_grad(sc, sm, sp, c0, r0, d, gl);
           tan_grad(sc, sm, sp, c1, r1, d, gh);
         }
-        phi_face(kp, lo, hi, ANISO ? gl : gdum, ANISO ? gh : gdum, d, jf);
+        phi_face<PF_AN>(kp, lo, hi, ANISO ? gl : gdum, ANISO ? gh : gdum, d, jf);
 #pragma unroll
         for (int a = 0; a < NPH; ++a) {
           if (d == 0) S.fx[fb][a][r0 - 1][TX] = jf[a];
@@ -190,7 +194,7 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
         if (ANISO) pc[a] = T(S.p[sc][a], orow, oc);
       }
       if (ANISO) tan_grad(sp, sp, sp, oc, orow, 2, gh);   // lo side: the own cell's gown
-      phi_face(kp, pc, pp, ANISO ? gown : gdum, ANISO ? gh : gdum, 2, jzp);
+      phi_face<PF_AN>(kp, pc, pp, ANISO ? gown : gdum, ANISO ? gh : gdum, 2, jzp);
 #pragma unroll
       for (int a = 0; a < NPH; ++a) {
         if (ANISO) continue;   // anisotropic: formed after the barrier (registers)
@@ -234,7 +238,7 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
         gc[a][1] = T(S.p[sc][a], orow + 1, oc) - T(S.p[sc][a], orow - 1, oc);
         gc[a][2] = pp[a] - T(S.p[sm][a], orow, oc);
       }
-      phi_cell_rhs0(kp, S.tab[sc], pc, mu_c, gc, r0);
+      phi_cell_rhs0<PF_AN>(kp, S.tab[sc], pc, mu_c, gc, r0);
       const double c = S.tab[sc][T_EPSTDX];
 #pragma unroll
       for (int a = 0; a < NPH; ++a) q[a] = r0[a] - c * dpart[a];
@@ -249,7 +253,7 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
       const double c = S.tab[sc][T_EPSTDX];
       if (ANISO) {
         double r0[NPH];
-        phi_cell_rhs0(kp, S.tab[sc], pc, mu_c, gown, r0);
+        phi_cell_rhs0<PF_AN>(kp, S.tab[sc], pc, mu_c, gown, r0);
 #pragma unroll
         for (int a = 0; a < NPH; ++a) {
           dpart[a] = (jzp[a] - S.jz[a][ty][tx]) - S.fx[fb][a][ty][tx] - S.fy[fb][a][ty][tx];
@@ -269,6 +273,7 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
       for (int a = 0; a < NPH; ++a) S.jz[a][ty][tx] = jzp[a];   // thread-private slot
   }
 #undef T
+#undef PF_AN
 }
 
 // Opt-in to > 48 KB of dynamic shared memory, once per process (pf_create;
