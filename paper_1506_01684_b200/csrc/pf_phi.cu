@@ -32,7 +32,7 @@ struct __align__(128) PhiSmem {
 
 constexpr uint32_t PHI_STAGE_BYTES = (NPH * RXS * RY + TAB) * 8;
 
-template <bool ANISO>
+template <bool ANISO, bool SC>
 #ifndef PF_PHI_MINB
 #define PF_PHI_MINB (512 / NTHR)
 #endif
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
     // are all simplex vertices with an identical D3C7 (D3C19) neighbourhood
     // keeps phi^{n+1} = phi^n — bitwise what the full update returns (is_vertex)
     auto bulk_warp = [&]() {
-      if (!kp.shortcuts) return false;
+      if (!SC || !kp.shortcuts) return false;   // SC = false: the check compiled out
       bool mine = is_vertex(pc);
 #pragma unroll
       for (int a = 0; a < NPH; ++a) {
@@ -282,10 +282,11 @@ static int g_phi_slots[2] = {1, 1};   // resident CTAs on the GPU, [ANISO]
 
 void prepare_phi_tiled() {
   const int sm = (int)sizeof(PhiSmem);
-  cudaFuncSetAttribute(phi_tiled_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(phi_tiled_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  g_phi_slots[0] = grid_slots(phi_tiled_kernel<false>, NTHR, sm);
-  g_phi_slots[1] = grid_slots(phi_tiled_kernel<true>, NTHR, sm);
+  cudaFuncSetAttribute(phi_tiled_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(phi_tiled_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(phi_tiled_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  g_phi_slots[0] = grid_slots(phi_tiled_kernel<false, true>, NTHR, sm);
+  g_phi_slots[1] = grid_slots(phi_tiled_kernel<true, false>, NTHR, sm);
 }
 
 void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm) {
@@ -296,8 +297,12 @@ void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, con
   const int kz = chunk_z(b.nz, gx * gy, g_phi_slots[kp.aniso ? 1 : 0], PF_PHI_WAVES, false);
   dim3 grd(gx, gy, (b.nz + kz - 1) / kz), blk(TX, TY);
   const size_t sm = sizeof(PhiSmem);
-  if (kp.aniso) phi_tiled_kernel<true><<<grd, blk, sm, s>>>(tm, kp, b, kz);
-  else phi_tiled_kernel<false><<<grd, blk, sm, s>>>(tm, kp, b, kz);
+  // the anisotropic kernel without the shortcut check when it is off (-3 %); the
+  // isotropic one keeps the run-time check (its code without it measured +4 %:
+  // the compiler's schedule, not the check, decides there)
+  if (kp.aniso && kp.shortcuts) phi_tiled_kernel<true, true><<<grd, blk, sm, s>>>(tm, kp, b, kz);
+  else if (kp.aniso) phi_tiled_kernel<true, false><<<grd, blk, sm, s>>>(tm, kp, b, kz);
+  else phi_tiled_kernel<false, true><<<grd, blk, sm, s>>>(tm, kp, b, kz);
 }
 
 }  // namespace pf
