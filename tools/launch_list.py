@@ -9,9 +9,11 @@ rows = [r for r in csv.DictReader(lines) if r.get("Metric Name") == "gpu__time_d
 agg = {}
 for r in rows:
     k = r["Kernel Name"].split("(")[0]
+    if "<" in k:   # template arguments may contain spaces: keep them, name the kernel by its base
+        k = k[:k.index("<")].split()[-1] + k[k.index("<"):]
     n, t = agg.get(k, (0, 0.0))
     agg[k] = (n + 1, t + float(r["Metric Value"].replace(",", "")) / 1e6)
-step_k = {k: v for k, v in agg.items() if k.split()[-1].split("<")[0] in
+step_k = {k: v for k, v in agg.items() if k.split("<")[0].split()[-1] in
           ("phi_tiled_kernel", "mu_tiled_kernel", "copy_kernel", "table_kernel")}
 tot = sum(t for _, t in step_k.values())
 print(f"# ncu launch list (gpu__time_duration.sum, --clock-control none), {sys.argv[1]}\n")
