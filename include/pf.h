@@ -185,11 +185,12 @@ pf_status pf_read(pf_ctx *c, double *phi, double *mu);
  * the result equals pf_write(phi_in, mu_in) + pf_step(1) + pf_read(phi_out,
  * mu_out) bit for bit, including the state left on the device (time level
  * n+1, all ghosts filled).  Layout above; the in and out arrays may be the
- * same (in place).  On a context with one block per process, no window, the
- * tiled sweeps and overlap 0 or 1, the block is cut into ~32 z-slabs: the
+ * same (in place).  On a context with one block per process, the tiled
+ * sweeps and overlap 0 or 1, the block is cut into ~32 z-slabs: the
  * upload of slab s+1, the sweeps of the slabs below it and the download of
  * finished slabs overlap (PCIe is full duplex; pinned host memory reaches its
- * bandwidth).  Otherwise it runs those three calls in order.  Does not need a
+ * bandwidth); a moving-window shift after the step reads the shifted state
+ * once more.  Otherwise it runs those three calls in order.  Does not need a
  * prior pf_init/pf_write.  Blocking.  Errors: PF_ERR_ARG (NULL pointer), as
  * pf_write / pf_step / pf_read. */
 pf_status pf_step_io(pf_ctx *c, const double *phi_in, const double *mu_in, double *phi_out, double *mu_out);

@@ -119,6 +119,7 @@ struct pf_ctx {
   // upload and download streams
   struct SlabIO {
     int H = 0, S = 0;                      // slab height, slab count
+    int woff = 0;                          // window offset the copy lists were built for
     std::vector<CopyOp *> ops[2][2];       // [field][copy][slab]
     std::vector<int> nops[2][2];
     std::vector<int64_t> nctas[2][2];
@@ -645,9 +646,13 @@ pf_status slab_ops(pf_ctx *c, int field, int copy, int z0, int z1, CopyOp **d, i
   return upload_ops(c, ops, d, nctas);
 }
 
+void slab_free(pf_ctx *c);
+
 pf_status slab_setup(pf_ctx *c) {
   auto &io = c->sio;
-  if (io.S) return PF_OK;
+  if (io.S && io.woff == c->blocks[0].woff) return PF_OK;
+  if (io.S) slab_free(c);   // the window moved since: the copy lists hold plane addresses
+  io.woff = c->blocks[0].woff;
   const int nz = c->blocks[0].nz;
 #ifndef PF_SLABS
 #define PF_SLABS 32   // measured at 512^3: 16 -> 151.9, 32 -> 147.3, 64 -> 150.7 ms per step
@@ -1316,7 +1321,7 @@ pf_status pf_step_io(pf_ctx *c, const double *phi_in, const double *mu_in, doubl
   // the slab pipeline covers one block per process, no window, the tiled
   // sweeps and the Algorithm-1 mu update (overlap 0 / 1 are bitwise equal);
   // anything else is the same sequence of calls without the overlap
-  if (!host || c->g.nranks != 1 || c->blocks.size() != 1 || c->p.window || c->p.variant == 1 ||
+  if (!host || c->g.nranks != 1 || c->blocks.size() != 1 || c->p.variant == 1 ||
       (c->p.overlap != 0 && c->p.overlap != 1)) {
     CKS(pf_write(c, phi_in, mu_in));
     CKS(pf_step(c, 1));
@@ -1367,7 +1372,13 @@ pf_status pf_step_io(pf_ctx *c, const double *phi_in, const double *mu_in, doubl
   c->cur ^= 1;
   c->step += 1;
   c->initialized = true;
+  // moving window (a new state: the front is checked now, as after pf_write +
+  // pf_step): a shift changes the state after its download, which is then
+  // read again — the rare step pays one more transfer
   c->next_check = c->step;
+  const int64_t shifts = c->shifts;
+  CKS(window_check(c));
+  if (c->shifts != shifts) CKS(move_state(c, phi_out, mu_out, false));
   if (c->p.nan_check_every > 0 && c->step % c->p.nan_check_every == 0) CKS(nan_check(c));
   return PF_OK;
 }

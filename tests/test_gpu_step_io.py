@@ -72,6 +72,24 @@ def test_step_io_in_place_trajectory(pv1):
     assert _equal((hphi, hmu), ref)
 
 
+def test_step_io_window_shifts(pv1):
+    # moving window with shifts during the run (front above 2/3 of the height):
+    # the streamed step re-reads the state a shift changed after its download
+    pf = _pf()
+    cfg, (phi, mu) = _state("c5", 24, 24, 24)
+    prm = pf.make_params(pv1, cfg, layer_height=17.5, window=True)
+    ha, ma, hb, mb = phi.copy(), mu.copy(), phi.copy(), mu.copy()
+    with pf.Context(24, 24, 24, prm) as a, pf.Context(24, 24, 24, prm) as b:
+        for _ in range(6):
+            a.step_io(ha, ma, ha, ma)
+            b.write(hb, mb)
+            b.step(1)
+            b.read(hb, mb)
+            assert _equal((ha, ma), (hb, mb))
+        assert a.info().shifts == b.info().shifts > 0
+        assert a.info().z_origin == b.info().z_origin
+
+
 @pytest.mark.parametrize("kw", [dict(blocks=(2, 1, 1)), dict(blocks=(1, 1, 2)), dict(window=True),
                                 dict(overlap=2)])
 def test_step_io_fallback_paths(pv1, kw):
