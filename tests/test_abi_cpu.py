@@ -65,3 +65,28 @@ def test_mesh_case_table_matches_oracle():
         ref = [tuple(tr) for tr in MC.cube_triangles([(case >> c) & 1 == 1 for c in range(8)])]
         got = [tuple(int(x) for x in t[case, 1 + 3 * i:4 + 3 * i]) for i in range(t[case, 0])]
         assert got == ref, case
+
+
+def test_create_validates_before_the_device():
+    # empty, degenerate and inconsistent configurations are rejected by
+    # pf_create's validation (PF_ERR_CONFIG, message in pf_last_error) before
+    # any device is touched, so this runs without a GPU
+    import pytest
+    from paper_1506_01684_b200 import pf
+    from inputs import gen
+    cfg = gen.load_config("c1")
+    good = dict(nx=16, ny=16, nz=16, blocks=(1, 1, 1))
+    cases = [(dict(nx=0), "axis x: non-positive"), (dict(nz=-4), "axis z: non-positive"),
+             (dict(ny=1), "axis y: blocks must be >= 2"), (dict(nx=16, blocks=(16, 1, 1)), "axis x: blocks must be >= 2"),
+             (dict(nz=15, blocks=(1, 1, 2)), "axis z: 15 cells not divisible")]
+    for over, msg in cases:
+        a = dict(good, **over)
+        prm = pf.make_params(gen.load_params("v1"), cfg)
+        with pytest.raises(pf.PfError) as e:
+            pf.Context(a["nx"], a["ny"], a["nz"], prm, *a["blocks"])
+        assert e.value.status == pf.PF_ERR_CONFIG and msg in str(e.value), (over, str(e.value))
+    prm = pf.make_params(gen.load_params("v1"), cfg)
+    prm.gamma[0][1] = 0.5 * prm.gamma[0][1]   # not symmetric any more
+    with pytest.raises(pf.PfError) as e:
+        pf.Context(16, 16, 16, prm)
+    assert e.value.status == pf.PF_ERR_CONFIG and "not symmetric" in str(e.value)
