@@ -78,6 +78,22 @@ def test_ragged_shapes(pv1, shape):
     assert O.rel_maxnorm(gmu, omu) <= TOL1
 
 
+@pytest.mark.parametrize("shape", [(2, 2, 2), (2, 5, 3), (3, 2, 7), (2, 2, 40)])
+@pytest.mark.parametrize("aniso", [False, True])
+def test_minimum_sizes(pv1, shape, aniso):
+    # the smallest blocks pf_create accepts (2 cells per axis): a tile is mostly
+    # inactive threads, the periodic ghosts are the other interior cell, a
+    # z-chunk may hold one plane
+    nx, ny, nz = shape
+    lh = nz / 2
+    cfg, (phi, mu) = _state("c2", nx, ny, nz, layer_height=lh, mu_noise=1e-2)
+    gphi, gmu, _ = _gpu_run(pv1, cfg, phi, mu, 3, aniso=aniso, delta_sl=0.05 if aniso else None, layer_height=lh)
+    ophi, omu, _ = O.run(_oracle_params(pv1, cfg, aniso=aniso, delta_sl=0.05 if aniso else None, layer_height=lh),
+                         phi, mu, 3)
+    assert O.rel_maxnorm(gphi, ophi) <= TOL1
+    assert O.rel_maxnorm(gmu, omu) <= TOL1
+
+
 @pytest.mark.parametrize("variant", [0, 1])
 def test_anisotropic(pv1, variant):
     cfg, (phi, mu) = _state("c5", 24, 20, 16, layer_height=8, n_seeds=6)
@@ -230,6 +246,46 @@ def _sample_cells(nx, ny, nz, m, seed=0):
     cells = [(k * ny + j) * nx + i for i, j, k in pts]
     cells += list(rng.integers(0, nx * ny * nz, m))
     return np.array(cells, dtype=np.int64)
+
+
+def test_c5_full_size_1024_sampled(pv1):
+    # C5 at its one-GPU size (1024^3, anisotropic, moving window) in bench.py's
+    # launch configuration: the state from pf_init (the generator's recipe on the
+    # device, <= 1e-15 from the host generator), one step, the result read into
+    # device memory and sampled; the oracle steps the same cells of a z-slab the
+    # host generator builds around the front, with the slab's origin as window
+    # origin (T(z) of the global planes) — cells >= 3 planes from the slab's ends
+    # see no difference from the whole domain (the step's reach is 2 planes)
+    import torch
+    pf = _pf()
+    cfg = gen.load_config("c5")
+    n = 1024
+    lh = int(cfg["init"]["layer_height"])
+    z0, nzs = lh - 11, 22
+    prm = pf.make_params(pv1, cfg, nx=n, ny=n)
+    rng = np.random.default_rng(5)
+    loc = np.stack([rng.integers(0, n, 4000), rng.integers(0, n, 4000), rng.integers(3, nzs - 3, 4000)])
+    cells = (loc[2] + z0) * n * n + loc[1] * n + loc[0]
+    with pf.Context(n, n, n, prm) as ctx:
+        ctx.init(cfg["seed"])
+        ctx.step(1)
+        assert ctx.info().shifts == 0
+        tp = torch.empty((4, n, n, n), dtype=torch.float64, device="cuda")
+        tm = torch.empty((2, n, n, n), dtype=torch.float64, device="cuda")
+        ctx.read(tp, tm)
+    idx = torch.from_numpy(cells).cuda()
+    gp = tp.reshape(4, -1)[:, idx].cpu().numpy()
+    gm = tm.reshape(2, -1)[:, idx].cpu().numpy()
+    del tp, tm
+    torch.cuda.empty_cache()
+    spec = gen.spec_from_config(cfg, n, n)
+    phi, mu = gen.generate(spec, n, n, n, box=(0, 0, z0, n, n, nzs))
+    op = _oracle_params(pv1, cfg)   # T0 from the global layer height; zorig = z0 places the planes
+    lc = loc[2] * n * n + loc[1] * n + loc[0]
+    po, mo = O.step_cells(op, phi, mu, lc, n=0, zorig=z0)
+    assert O.rel_maxnorm(gp, po) <= TOL1
+    assert O.rel_maxnorm(gm, mo) <= TOL1
+    assert np.abs(po - phi.reshape(4, -1)[:, lc]).max() > 1e-6   # the sample sees the front move
 
 
 def test_c2_full_one_step(pv1):
