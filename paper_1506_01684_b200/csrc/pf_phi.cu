@@ -152,6 +152,29 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
     if (ANISO) tan_grad(sc, sm, sp, oc, orow, -1, gown);
     {
       double jf[NPH], lo[NPH], hi[NPH], gl[NPH][3], gh[NPH][3];
+      // far faces: +y of the last row, +x of the last column (warp 0); the
+      // isotropic kernel issues them first, the anisotropic one after its own
+      // faces (measured: iso -1.1 %, aniso +5 % the other way round)
+      auto far_faces = [&]() {
+        if (tid < TX + TY) {
+          const int d = tid < TX ? 1 : 0;
+          const int c0 = d == 1 ? tid + 1 : TX, r0 = d == 1 ? TY : tid - TX + 1;
+          const int c1 = d == 1 ? c0 : c0 + 1, r1 = d == 1 ? r0 + 1 : r0;
+#pragma unroll
+          for (int a = 0; a < NPH; ++a) { lo[a] = T(S.p[sc][a], r0, c0); hi[a] = T(S.p[sc][a], r1, c1); }
+          if (ANISO) {
+            tan_grad(sc, sm, sp, c0, r0, d, gl);
+            tan_grad(sc, sm, sp, c1, r1, d, gh);
+          }
+          phi_face<PF_AN>(kp, lo, hi, ANISO ? gl : gdum, ANISO ? gh : gdum, d, jf);
+#pragma unroll
+          for (int a = 0; a < NPH; ++a) {
+            if (d == 0) S.fx[fb][a][r0 - 1][TX] = jf[a];
+            else S.fy[fb][a][TY][c0 - 1] = jf[a];
+          }
+        }
+      };
+      if (!ANISO) far_faces();
 #pragma unroll
       for (int d = 0; d < 2; ++d) {   // own -x (d = 0) and -y (d = 1) face
         const int lc = d == 0 ? oc - 1 : oc, lr = d == 0 ? orow : orow - 1;
@@ -169,24 +192,7 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
           if (!ANISO) dpart[a] = d == 0 ? -jf[a] : dpart[a] - jf[a];
         }
       }
-      // far faces: +y of the last row (warp 0), +x of the last column (warp 1)
-      if (tid < TX + TY) {
-        const int d = tid < TX ? 1 : 0;
-        const int c0 = d == 1 ? tid + 1 : TX, r0 = d == 1 ? TY : tid - TX + 1;
-        const int c1 = d == 1 ? c0 : c0 + 1, r1 = d == 1 ? r0 + 1 : r0;
-#pragma unroll
-        for (int a = 0; a < NPH; ++a) { lo[a] = T(S.p[sc][a], r0, c0); hi[a] = T(S.p[sc][a], r1, c1); }
-        if (ANISO) {
-          tan_grad(sc, sm, sp, c0, r0, d, gl);
-          tan_grad(sc, sm, sp, c1, r1, d, gh);
-        }
-        phi_face<PF_AN>(kp, lo, hi, ANISO ? gl : gdum, ANISO ? gh : gdum, d, jf);
-#pragma unroll
-        for (int a = 0; a < NPH; ++a) {
-          if (d == 0) S.fx[fb][a][r0 - 1][TX] = jf[a];
-          else S.fy[fb][a][TY][c0 - 1] = jf[a];
-        }
-      }
+      if (ANISO) far_faces();
       // z-face k+1/2 (own column)
 #pragma unroll
       for (int a = 0; a < NPH; ++a) {
