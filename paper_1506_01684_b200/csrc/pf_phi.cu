@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
     // once (the LSU pipe, not the FP64 pipe, was the busier one: ncu v14 72 %
     // vs 58 %) and, isotropic, the cell's own faces enter its divergence from
     // registers before the barrier:
-    //   dpart = (jz+ - jz-) - jx- - jy-,   rhs = (r0 - c dpart) - c (jx+ + jy+)
+    //   dpart = ((jz+ - jz-) - jx-) - jy-,   rhs = (r0 - c dpart) - c (jx+ + jy+)
     // with c = eps T / dx (the oracle's O4.6 sum in another order: equal up to
     // rounding; the anisotropic kernel forms dpart after the barrier).
     double pc[NPH], pp[NPH], jzp[NPH], dpart[NPH];
@@ -175,6 +175,16 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
         }
       };
       if (!ANISO) far_faces();
+      if (!ANISO) {   // isotropic: the z-face k+1/2 next (measured -0.8 % against last)
+#pragma unroll
+        for (int a = 0; a < NPH; ++a) pp[a] = T(S.p[sp][a], orow, oc);
+        phi_face<PF_AN>(kp, pc, pp, gdum, gdum, 2, jzp);
+#pragma unroll
+        for (int a = 0; a < NPH; ++a) {
+          dpart[a] = jzp[a] - jzm[a];
+          jzm[a] = jzp[a];
+        }
+      }
 #pragma unroll
       for (int d = 0; d < 2; ++d) {   // own -x (d = 0) and -y (d = 1) face
         const int lc = d == 0 ? oc - 1 : oc, lr = d == 0 ? orow : orow - 1;
@@ -189,23 +199,18 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
         for (int a = 0; a < NPH; ++a) {
           if (d == 0) S.fx[fb][a][ty][tx] = jf[a];
           else S.fy[fb][a][ty][tx] = jf[a];
-          if (!ANISO) dpart[a] = d == 0 ? -jf[a] : dpart[a] - jf[a];
+          if (!ANISO) dpart[a] -= jf[a];
         }
       }
       if (ANISO) far_faces();
-      // z-face k+1/2 (own column)
+      if (ANISO) {   // anisotropic: the z-face k+1/2 last (its dpart is formed after the barrier)
 #pragma unroll
-      for (int a = 0; a < NPH; ++a) {
-        pp[a] = T(S.p[sp][a], orow, oc);
-        if (ANISO) pc[a] = T(S.p[sc][a], orow, oc);
-      }
-      if (ANISO) tan_grad(sp, sp, sp, oc, orow, 2, gh);   // lo side: the own cell's gown
-      phi_face<PF_AN>(kp, pc, pp, ANISO ? gown : gdum, ANISO ? gh : gdum, 2, jzp);
-#pragma unroll
-      for (int a = 0; a < NPH; ++a) {
-        if (ANISO) continue;   // anisotropic: formed after the barrier (registers)
-        dpart[a] += jzp[a] - jzm[a];
-        jzm[a] = jzp[a];
+        for (int a = 0; a < NPH; ++a) {
+          pp[a] = T(S.p[sp][a], orow, oc);
+          pc[a] = T(S.p[sc][a], orow, oc);
+        }
+        tan_grad(sp, sp, sp, oc, orow, 2, gh);   // lo side: the own cell's gown
+        phi_face<PF_AN>(kp, pc, pp, gown, gh, 2, jzp);
       }
     }
     // region shortcut (NEXT-1): a warp whose cells
