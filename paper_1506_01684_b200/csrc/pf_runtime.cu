@@ -655,10 +655,10 @@ pf_status slab_setup(pf_ctx *c) {
   io.woff = c->blocks[0].woff;
   const int nz = c->blocks[0].nz;
 #ifndef PF_SLABS
-#define PF_SLABS 32   // measured at 512^3: 16 -> 151.9, 32 -> 147.3, 64 -> 150.7 ms per step
+#define PF_SLABS 32   // measured at 512^3: 16 -> 146.1, 32 -> 144.4, 64 -> 146.1 ms per step
 #endif
-  // ~PF_SLABS slabs: the download of slab s waits for the upload of slab s+2,
-  // so the pipeline's fill + drain cost ~4 slabs of one-way transfer time
+  // ~PF_SLABS slabs: the download of slab s waits for the upload of slab s+1,
+  // so the pipeline's fill + drain cost ~2 slabs of one-way transfer time
   io.H = std::max(4, (nz + PF_SLABS - 1) / PF_SLABS);
   io.S = (nz + io.H - 1) / io.H;
   CK(cudaStreamCreateWithFlags(&io.up, cudaStreamNonBlocking));
