@@ -175,6 +175,15 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
         }
       };
       if (!ANISO) far_faces();
+      if (ANISO) {   // anisotropic: the z-face k+1/2 first too (its dpart is formed after the barrier; -0.4 %)
+#pragma unroll
+        for (int a = 0; a < NPH; ++a) {
+          pp[a] = T(S.p[sp][a], orow, oc);
+          pc[a] = T(S.p[sc][a], orow, oc);
+        }
+        tan_grad(sp, sp, sp, oc, orow, 2, gh);   // lo side: the own cell's gown
+        phi_face<PF_AN>(kp, pc, pp, gown, gh, 2, jzp);
+      }
       if (!ANISO) {   // isotropic: the z-face k+1/2 next (measured -0.8 % against last)
 #pragma unroll
         for (int a = 0; a < NPH; ++a) pp[a] = T(S.p[sp][a], orow, oc);
@@ -203,15 +212,6 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
         }
       }
       if (ANISO) far_faces();
-      if (ANISO) {   // anisotropic: the z-face k+1/2 last (its dpart is formed after the barrier)
-#pragma unroll
-        for (int a = 0; a < NPH; ++a) {
-          pp[a] = T(S.p[sp][a], orow, oc);
-          pc[a] = T(S.p[sc][a], orow, oc);
-        }
-        tan_grad(sp, sp, sp, oc, orow, 2, gh);   // lo side: the own cell's gown
-        phi_face<PF_AN>(kp, pc, pp, gown, gh, 2, jzp);
-      }
     }
     // region shortcut (NEXT-1): a warp whose cells
     // are all simplex vertices with an identical D3C7 (D3C19) neighbourhood
