@@ -23,13 +23,18 @@
  * from the same source.  Quantities that depend on T only (the per-plane
  * values) are plain doubles and are not counted.
  *
- * Pins (tests/test_oracle_*.py): P1 analytic profile, P2 textbook binary
+ * Pins (tests/test_oracle_pins.py): P1 analytic profile, P2 textbook binary
  * reduction, P3 simplex + active-set enumeration, P4 solute conservation,
  * P5 Fourier decay, P6 permutation symmetry, P7 bulk fixed point, P8 term
  * identities, P10 anti-trapping zeros, P11 single-face anti-trapping
- * properties, P12 undercooling sign, P13 cubic symmetry.  The coupled
- * multi-phase phi-mu-J_at regime beyond those pins is "parity unpinned"
- * (DESIGN.md §5).
+ * properties, P12 undercooling sign, P13 cubic symmetry, P17 window
+ * transparency, P18 mirror symmetry, P19 dc/dT source vs the exact solution
+ * of a temperature-driven liquid (kappa and m terms), P20 face gradients exact
+ * on linear fields (D3C19 tangential averages in J_at and the anisotropic phi
+ * faces), P21 homogeneity of the cubic gradient energy.  The coupled
+ * multi-phase phi-mu-J_at regime beyond those pins is guarded by the second,
+ * independent NumPy coding (oracle/oracle_np.py, tests/test_oracle_second_coding.py)
+ * and by tools/oracle_mutants.py (every listed slip fails a pin).
  */
 #include <algorithm>
 #include <cmath>
@@ -173,32 +178,60 @@ template <class R> inline void interp_h(const R ph[N], R h[N]) {
 /* q_ab = phi_a grad phi_b - phi_b grad phi_a (reading R3);       */
 /* e(q) and g(q) = de/dq.  a_c = 1 - delta(3-4Q4/|q|^4) */
 /* ------------------------------------------------------------------------ */
-template <class R> inline R pair_energy(const or_params &p, int a, int b, const R q[3]) {
+/* Cubic anisotropy a_c depends on q/|q| only, so e is homogeneous of degree 2
+ * and g of degree 1 in q.  Both are evaluated on u = q 2^-s, max|u_d| in
+ * [1/2, 1) (s from frexp), and scaled back by 2^(2s) / 2^s: a power-of-two
+ * scaling is exact, so in the normal range the result has the bits of the
+ * unscaled formula, and q^6 no longer under- or overflows for tiny or huge
+ * |q| (g(q) -> 0 continuously as q -> 0). */
+inline double ldexp_r(double x, int s) { return std::ldexp(x, s); }
+inline Counted ldexp_r(Counted x, int s) { return Counted(std::ldexp(x.v, s)); }  /* exact: not a FLOP */
+template <class R> inline int pow2_scale(const R q[3]) {
+  const double m = std::max(std::fabs(val(q[0])), std::max(std::fabs(val(q[1])), std::fabs(val(q[2]))));
+  int s = 0;
+  std::frexp(m, &s);
+  return s;
+}
+template <class R> inline R pair_energy(const or_params &p, int a, int b, const R q_[3]) {
+  if (q_[0] == 0.0 && q_[1] == 0.0 && q_[2] == 0.0) return R(0.0);
+  const int s = p.aniso ? pow2_scale(q_) : 0;
+  R q[3];
+  for (int d = 0; d < 3; ++d) q[d] = ldexp_r(q_[d], -s);
   const R q2 = q[0] * q[0] + q[1] * q[1] + q[2] * q[2];
-  if (q2 == 0.0) return R(0.0);
   R ac = R(1.0);
   if (p.aniso) {
     const R Q4 = q[0] * q[0] * q[0] * q[0] + q[1] * q[1] * q[1] * q[1] + q[2] * q[2] * q[2] * q[2];
     ac = R(1.0) - R(p.delta[a][b]) * (R(3.0) - R(4.0) * Q4 / (q2 * q2));
   }
-  return R(p.gamma[a][b]) * ac * ac * q2;
+  return ldexp_r(R(p.gamma[a][b]) * ac * ac * q2, 2 * s);
 }
-template <class R> inline void pair_grad(const or_params &p, int a, int b, const R q[3], R gq[3]) {
+/* Components d in [d0, d1) of g_ab(q) (the face fluxes need only the normal
+ * component d, the centre term all three). */
+template <class R> inline void pair_grad_range(const or_params &p, int a, int b, const R q_[3], R gq[3], int d0, int d1) {
   if (!p.aniso) {  /* e = gamma |q|^2  ->  g = 2 gamma q */
-    for (int d = 0; d < 3; ++d) gq[d] = R(2.0 * p.gamma[a][b]) * q[d];
+    for (int d = d0; d < d1; ++d) gq[d] = R(2.0 * p.gamma[a][b]) * q_[d];
     return;
   }
+  if (q_[0] == 0.0 && q_[1] == 0.0 && q_[2] == 0.0) {  /* g(0) = 0 */
+    for (int d = d0; d < d1; ++d) gq[d] = R(0.0);
+    return;
+  }
+  const int s = pow2_scale(q_);
+  R q[3];
+  for (int d = 0; d < 3; ++d) q[d] = ldexp_r(q_[d], -s);
   const R q2 = q[0] * q[0] + q[1] * q[1] + q[2] * q[2];
-  if (q2 == 0.0) { gq[0] = gq[1] = gq[2] = R(0.0); return; }  /* g(0) = 0 */
   /* d a_c / d q_d = 16 delta (q_d^3/|q|^4 - Q4 q_d/|q|^6);
      g_d = 2 gamma a_c ( |q|^2 d a_c/d q_d + a_c q_d ) */
   const R Q4 = q[0] * q[0] * q[0] * q[0] + q[1] * q[1] * q[1] * q[1] + q[2] * q[2] * q[2] * q[2];
   const R q4 = q2 * q2;
   const R ac = R(1.0) - R(p.delta[a][b]) * (R(3.0) - R(4.0) * Q4 / q4);
-  for (int d = 0; d < 3; ++d) {
+  for (int d = d0; d < d1; ++d) {
     const R dac = R(16.0 * p.delta[a][b]) * (q[d] * q[d] * q[d] / q4 - Q4 * q[d] / (q4 * q2));
-    gq[d] = R(2.0 * p.gamma[a][b]) * ac * (q2 * dac + ac * q[d]);
+    gq[d] = ldexp_r(R(2.0 * p.gamma[a][b]) * ac * (q2 * dac + ac * q[d]), s);
   }
+}
+template <class R> inline void pair_grad(const or_params &p, int a, int b, const R q[3], R gq[3]) {
+  pair_grad_range(p, a, b, q, gq, 0, 3);
 }
 
 /* O4.7 multi-obstacle potential (reading
@@ -232,13 +265,14 @@ template <class R> inline R domega(const or_params &p, const R ph[N], int a) {
 }
 
 /* O4.8 driving force d psi / d phi_a = sum_b psi_b dh_b/dphi_a
- *      = (2 phi_a / S)(psi_a - sum_b h_b psi_b) */
-template <class R> inline R dpsi_dphi(const R ph[N], const R ps[N], int a) {
+ *      = (2 phi_a / S)(psi_a - psibar), psibar = sum_b h_b psi_b,
+ *      S and psibar formed once per cell */
+template <class R> inline void dpsi_dphi_all(const R ph[N], const R ps[N], R out[N]) {
   R S = ph[0] * ph[0];
   for (int b = 1; b < N; ++b) S = S + ph[b] * ph[b];
   R pbar = R(0.0);
   for (int b = 0; b < N; ++b) pbar = pbar + ph[b] * ph[b] / S * ps[b];
-  return R(2.0) * ph[a] / S * (ps[a] - pbar);
+  for (int a = 0; a < N; ++a) out[a] = R(2.0) * ph[a] / S * (ps[a] - pbar);
 }
 
 /* O4.1 centre gradients (D3C7 central differences) of all phases */
@@ -276,7 +310,7 @@ inline void phi_face(const or_params &p, const R plo[N], const R phi_[N],
       R q[3], gq[3];
       if (p.aniso) {
         for (int e = 0; e < 3; ++e) q[e] = pb[a] * gf[b][e] - pb[b] * gf[a][e];
-        pair_grad(p, a, b, q, gq);
+        pair_grad_range(p, a, b, q, gq, d, d + 1);   /* the flux needs g_d only */
       } else {  /* isotropic: only the normal component of q and g is needed */
         gq[d] = R(2.0 * p.gamma[a][b]) * (pb[a] * gf[b][d] - pb[b] * gf[a][d]);
       }
@@ -354,10 +388,11 @@ void phi_cell(const or_params &p, const or_dims &g, const F &phi, const F &mu,
   }
 
   /* O4.7-9: rhs_a = eps T (da/dphi_a - div_a) + (T/eps) domega_a + dpsi_a */
-  R ps[N], rhs[N];
+  R ps[N], dps[N], rhs[N];
   for (int a = 0; a < N; ++a) ps[a] = psi(p, a, m, T);
+  dpsi_dphi_all(ph, ps, dps);
   for (int a = 0; a < N; ++a)
-    rhs[a] = R(p.eps * T) * (dadphi[a] - div[a]) + R(T / p.eps) * domega(p, ph, a) + dpsi_dphi(ph, ps, a);
+    rhs[a] = R(p.eps * T) * (dadphi[a] - div[a]) + R(T / p.eps) * domega(p, ph, a) + dps[a];
 
   /* O4.10: explicit Euler of Eq. (1) (minus sign), mean over all N phases */
   R mean = R(0.0);
@@ -409,10 +444,9 @@ template <class R>
 void mu_face(const or_params &p, const MuCellQ<R> &lo, const MuCellQ<R> &hi, int d, R F[NC], R J[NC]) {
   for (int c = 0; c < NC; ++c)
     F[c] = (lo.M[c] + hi.M[c]) / R(2.0) * (hi.mu[c] - lo.mu[c]) / R(p.dx);
-  R pb[N], gf[N][3], pd[N];
+  R pb[N], gf[N][3];
   for (int a = 0; a < N; ++a) {
     pb[a] = (lo.pn[a] + hi.pn[a]) / R(2.0);
-    pd[a] = (lo.dphi[a] + hi.dphi[a]) / R(2.0) / R(p.dt);
     for (int e = 0; e < 3; ++e)
       gf[a][e] = (e == d) ? (hi.pn[a] - lo.pn[a]) / R(p.dx) : (lo.gn[a][e] + hi.gn[a][e]) / R(2.0);
   }
@@ -420,17 +454,25 @@ void mu_face(const or_params &p, const MuCellQ<R> &lo, const MuCellQ<R> &hi, int
   for (int b = 1; b < N; ++b) S = S + pb[b] * pb[b];
   const R hl = pb[LIQ] * pb[LIQ] / S;
   const R gl2 = gf[LIQ][0] * gf[LIQ][0] + gf[LIQ][1] * gf[LIQ][1] + gf[LIQ][2] * gf[LIQ][2];
+  R nl[3];   /* liquid normal, once per face (only used when gl2 != 0) */
+  if (!(gl2 == 0.0)) {
+    const R nl_abs = sqrt(gl2);
+    for (int e = 0; e < 3; ++e) nl[e] = gf[LIQ][e] / nl_abs;
+  }
   for (int c = 0; c < NC; ++c) J[c] = R(0.0);
   for (int a = 0; a < N; ++a) {
     if (a == LIQ) continue;  /* sum over solids only (reading R24) */
+    const R pd = (lo.dphi[a] + hi.dphi[a]) / R(2.0) / R(p.dt);   /* face d phi_a / dt */
     const R pal = pb[a] * pb[LIQ];
     const R ga2 = gf[a][0] * gf[a][0] + gf[a][1] * gf[a][1] + gf[a][2] * gf[a][2];
-    if (pal == 0.0 || ga2 == 0.0 || gl2 == 0.0 || pd[a] == 0.0) continue;
-    const R na_abs = sqrt(ga2), nl_abs = sqrt(gl2);
+    if (pal == 0.0 || ga2 == 0.0 || gl2 == 0.0 || pd == 0.0) continue;
+    const R na_abs = sqrt(ga2);
+    R na[3];
+    for (int e = 0; e < 3; ++e) na[e] = gf[a][e] / na_abs;
     R dot = R(0.0);
-    for (int e = 0; e < 3; ++e) dot = dot + (gf[a][e] / na_abs) * (gf[LIQ][e] / nl_abs);
+    for (int e = 0; e < 3; ++e) dot = dot + na[e] * nl[e];
     /* (pi eps / 4) g_a h_l / sqrt(phi_a phi_l) dphi_a/dt (n_a . n_l) n_a,d */
-    const R w = R(M_PI * p.eps / 4.0) * (pb[a] * hl / sqrt(pal)) * pd[a] * dot * (gf[a][d] / na_abs);
+    const R w = R(M_PI * p.eps / 4.0) * (pb[a] * hl / sqrt(pal)) * pd * dot * na[d];
     for (int c = 0; c < NC; ++c) {
       /* (c^l - c^a) averaged over the two cells */
       const R dc = ((lo.cc[LIQ][c] - lo.cc[a][c]) + (hi.cc[LIQ][c] - hi.cc[a][c])) / R(2.0);
@@ -590,13 +632,29 @@ void or_interp_h(const double ph[4], double h[4]) { interp_h<double>(ph, h); }
 double or_omega(const or_params *p, const double ph[4]) { return omega<double>(*p, ph); }
 double or_domega(const or_params *p, const double ph[4], int a) { return domega<double>(*p, ph, a); }
 double or_dpsi_dphi(const or_params *p, const double ph[4], const double mu[2], double T, int a) {
-  double ps[N];
+  double ps[N], out[N];
   for (int b = 0; b < N; ++b) ps[b] = psi<double>(*p, b, mu, T);
-  return dpsi_dphi<double>(ph, ps, a);
+  dpsi_dphi_all<double>(ph, ps, out);
+  return out[a];
 }
 double or_pair_energy(const or_params *p, int a, int b, const double q[3]) { return pair_energy<double>(*p, a, b, q); }
 void or_pair_grad(const or_params *p, int a, int b, const double q[3], double gq[3]) { pair_grad<double>(*p, a, b, q, gq); }
 void or_project(const double x[4], double out[4]) { project_simplex<double>(x, out); }
+
+/* phi face flux j_a (O4.5) between global cell (i,j,k) and (i,j,k)+e_d, with
+ * both cells' centre gradients (the anisotropic tangential components). */
+int or_phi_face(const or_params *p, const or_dims *g, const double *phi, int64_t i, int64_t j, int64_t k,
+                int d, double jf[4]) {
+  const GlobalField F{phi, g};
+  int64_t di, dj, dk; unit(d, di, dj, dk);
+  double lo[N], hi[N], gl[N][3], gh[N][3];
+  load4(F, i, j, k, lo);
+  load4(F, i + di, j + dj, k + dk, hi);
+  centre_grad(*p, F, i, j, k, gl);
+  centre_grad(*p, F, i + di, j + dj, k + dk, gh);
+  phi_face<double>(*p, lo, hi, gl, gh, d, jf);
+  return 0;
+}
 
 /* Face (M grad mu) and J_at between global cell (i,j,k) and (i,j,k)+e_d. */
 int or_mu_face(const or_params *p, const or_dims *g, const double *phi_old, const double *phi_new,

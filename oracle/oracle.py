@@ -38,6 +38,10 @@ class OrDims(ctypes.Structure):
 
 
 def build(force: bool = False) -> str:
+    # PF_ORACLE_LIB: a prebuilt copy (tools/oracle_mutants.py loads mutated
+    # builds through it to show which pin catches each mutation)
+    if os.environ.get("PF_ORACLE_LIB"):
+        return os.environ["PF_ORACLE_LIB"]
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         subprocess.check_call(["g++", "-std=c++17", "-O2", "-fno-fast-math", "-ffp-contract=off",
                                "-fopenmp", "-shared", "-fPIC", "-o", _LIB, _SRC])
@@ -71,6 +75,8 @@ def lib():
         L.or_pair_energy.restype = D
         L.or_pair_grad.argtypes = [P, ctypes.c_int, ctypes.c_int, dp, dp]
         L.or_project.argtypes = [dp, dp]
+        if hasattr(L, "or_phi_face"):
+            L.or_phi_face.argtypes = [P, Dm, vp, I64, I64, I64, ctypes.c_int, dp]
         L.or_mu_face.argtypes = [P, Dm, vp, vp, vp, I64, I64, I64, ctypes.c_int, dp, dp]
         L.or_count_flops.argtypes = [P, ctypes.POINTER(I64)]
         _lib = L
@@ -249,6 +255,15 @@ def mu_face(p, phi_old, phi_new, mu, i, j, k, d, n=0, zorig=0):
     lib().or_mu_face(ctypes.byref(p), ctypes.byref(g), a, b, c, i, j, k, d,
                      F.ctypes.data_as(ctypes.POINTER(D)), J.ctypes.data_as(ctypes.POINTER(D)))
     return F, J
+
+
+def phi_face(p, phi, i, j, k, d, n=0, zorig=0):
+    """O4.5 face flux j_a between cell (i,j,k) and (i,j,k)+e_d (global indices)."""
+    phi, pp = _c(phi)
+    g = dims(phi.shape[3], phi.shape[2], phi.shape[1], n, zorig)
+    jf = np.zeros(4)
+    lib().or_phi_face(ctypes.byref(p), ctypes.byref(g), pp, i, j, k, d, jf.ctypes.data_as(ctypes.POINTER(D)))
+    return jf
 
 
 def count_flops(p: OrParams) -> dict:

@@ -386,33 +386,8 @@ def test_full_size_one_step_map_at_run_end(pv1, name, shape, steps):
 
 
 def _crafted(kind, nx, ny, nz, seed):
-    """Admissible crafted states (SURVEY.md §4 layer 3): every phase vector on
-    the Gibbs simplex; mu in [-0.3, 0.3]."""
-    rng = np.random.default_rng(seed)
-    mu = rng.uniform(-0.3, 0.3, (2, nz, ny, nx))
-    if kind == "random":          # every face a multi-phase interface: all anti-trapping guards open
-        phi = rng.random((4, nz, ny, nx)) ** 3
-        phi[rng.random((4, nz, ny, nx)) < 0.2] = 0.0
-        phi[3] += 1e-3                # no empty cell
-    elif kind == "triple":        # three phases meeting along z-lines + liquid above
-        x, y = np.meshgrid(np.arange(nx) + 0.5, np.arange(ny) + 0.5)
-        ang = np.arctan2(y - ny / 2, x - nx / 2)
-        phi = np.zeros((4, nz, ny, nx))
-        for a in range(3):
-            w = np.clip(1.0 - np.abs(((ang - 2 * np.pi * a / 3 + np.pi) % (2 * np.pi)) - np.pi) / (np.pi / 1.5), 0, 1)
-            phi[a] = w[None]
-        z = np.arange(nz)[:, None, None] + 0.5
-        s = np.clip(0.5 + (nz / 2 - z) / 4, 0, 1)
-        phi[:3] *= s
-        phi[3] = 1 - s + 1e-3
-    else:                         # binary 1D alpha|liquid front along x
-        x = np.arange(nx) + 0.5
-        r = np.clip(0.5 + (nx / 2 - x) / 4, 0, 1)
-        phi = np.zeros((4, nz, ny, nx))
-        phi[0] = r[None, None, :]
-        phi[3] = 1 - r[None, None, :]
-    phi /= phi.sum(axis=0, keepdims=True)
-    return phi, mu
+    from crafted import crafted
+    return crafted(kind, nx, ny, nz, seed)
 
 
 @pytest.mark.parametrize("kind", ["random", "triple", "binary"])

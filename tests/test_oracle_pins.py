@@ -742,3 +742,157 @@ def test_p18_mirror_symmetry(pv1, aniso):
         b, mb, _ = O.run(p, mr(phi), mr(mu), 10)
         assert np.abs(mr(b) - a).max() <= 1e-14, axis
         assert np.abs(mr(mb) - ma).max() <= 1e-14, axis
+
+
+# --------------------------------------------------------------------------
+# P19 — the dc/dT source of Eq. (3) against the exact solution of the
+# temperature-driven liquid (north_star "dT/dt source term")
+# --------------------------------------------------------------------------
+def _kappa_run(pd, T0, mu0, dt, t_end):
+    p = O.make_params(dict(pd, dt=dt), T0=T0)
+    phi = np.zeros((4, 1, 2, 2))
+    phi[3] = 1.0
+    mu = np.empty((2, 1, 2, 2))
+    mu[0], mu[1] = mu0
+    nsteps = int(round(t_end / dt))
+    ph, m, _ = O.run(p, phi, mu, nsteps)
+    assert np.array_equal(ph, phi)           # bulk liquid stays a vertex (P7)
+    return m[:, 0, 0, 0]
+
+
+@pytest.mark.parametrize("m_l", [[0.2, -0.1], [0.0, 0.0]])
+def test_p19_dcdT_source_converges_to_exact_solution(pv1, m_l):
+    # One uniform liquid layer (no gradients, no phase change) under a moving
+    # frozen temperature: Eq. (3) reduces to chi dmu/dt = -(dc/dT) dT/dt, whose
+    # exact solution conserves c = mu/(2A(T)) + c_hat(T):
+    #   mu(t) = 2 A(T(t)) (c_0 - c_hat(T(t))),  T(t) = T0 + G (z - v t).
+    # With m = 0 it is mu(t) = mu_0 A(T(t))/A(T_0), linear in t, and explicit
+    # Euler reproduces it exactly (mu^n = K A^n => mu^{n+1} = K A^{n+1}): only
+    # the kappa = 2 A1/(2A)^2 term of dc/dT drives it.  With m != 0 mu(t) is
+    # quadratic in t and Euler converges at first order in dt.
+    pd = dict(pv1, G=0.1, v=1.0, m=[list(r) for r in pv1["m"][:3]] + [m_l])
+    T0, mu0, t_end = pv1["T_eut"] + 0.02, np.array([0.4, -0.3]), 2.0
+    z = 0.5                                   # cell-centre height of plane 0
+
+    def exact(t):
+        T = T0 + pd["G"] * (z - pd["v"] * t)
+        th0, th = T0 + pd["G"] * z - pd["T_eut"], T - pd["T_eut"]
+        out = np.empty(2)
+        for c in range(2):
+            A_0 = pd["A0"][3][c] + pd["A1"][3][c] * th0
+            A_t = pd["A0"][3][c] + pd["A1"][3][c] * th
+            c0 = mu0[c] / (2 * A_0) + pd["c0"][3][c] + pd["m"][3][c] * th0
+            out[c] = 2 * A_t * (c0 - (pd["c0"][3][c] + pd["m"][3][c] * th))
+        return out
+
+    ref = exact(t_end)
+    assert np.abs(ref - mu0).max() > 1e-2     # the source moves mu by O(1e-2)
+    errs = [np.abs(_kappa_run(pd, T0, mu0, dt, t_end) - ref).max() for dt in (0.02, 0.01, 0.005)]
+    if m_l == [0.0, 0.0]:
+        assert max(errs) <= 1e-14, errs
+    else:
+        assert errs[2] <= 1e-3, errs
+        for e1, e2 in zip(errs, errs[1:]):
+            assert 1.9 <= e1 / e2 <= 2.1, errs    # first order in dt
+
+
+# --------------------------------------------------------------------------
+# P20 — face gradients are exact for linear fields (D3C19 tangential averages,
+# reading R4 / SURVEY.md §8(c) O4.5, O5.8): the discrete anti-trapping current
+# and the anisotropic phi face flux then equal their continuous formulas at
+# the face centre
+# --------------------------------------------------------------------------
+def _linear_phi(n, grads, base, centre):
+    """phi_a = base_a + grads_a . (x - centre) on an n^3 grid (cell centres at
+    integer indices), phi_l = 1 - sum of the solids."""
+    k, j, i = np.meshgrid(*(np.arange(n),) * 3, indexing="ij")
+    phi = np.zeros((4, n, n, n))
+    for a in range(3):
+        g = grads[a]
+        phi[a] = base[a] + g[0] * (i - centre[0]) + g[1] * (j - centre[1]) + g[2] * (k - centre[2])
+    phi[3] = 1.0 - phi[:3].sum(0)
+    return phi
+
+
+def test_p20_antitrapping_exact_on_linear_fields(pv1):
+    n, c = 9, (4, 4, 4)
+    grads = [np.array([0.010, 0.020, -0.015]), np.array([-0.012, 0.008, 0.011]), np.zeros(3)]
+    base = [0.30, 0.20, 0.05]
+    new = _linear_phi(n, grads, base, c)
+    old = _linear_phi(n, grads, [0.30 - 0.004, 0.20 + 0.003, 0.05], c)   # d phi/dt uniform per phase
+    assert new.min() > 0 and old.min() > 0
+    rng = np.random.default_rng(3)
+    mu = rng.uniform(-0.2, 0.2, (2, n, n, n))
+    pd = dict(pv1, G=0.01, v=0.3)
+    p = O.make_params(pd, layer_height=2.0)
+    step_n, zorig = 4, 1
+    gl = -(grads[0] + grads[1] + grads[2])           # liquid gradient
+    for d in range(3):
+        e = np.eye(3, dtype=int)[d]
+        lo = np.array(c)
+        hi = lo + e
+        xf = lo + 0.5 * e                            # face centre
+        ph = np.array([base[a] + grads[a] @ (xf - c) for a in range(3)])
+        ph = np.append(ph, 1.0 - ph.sum())
+        hl = ph[3] ** 2 / (ph ** 2).sum()
+        nl = gl / np.linalg.norm(gl)
+        expect = np.zeros(2)
+        for a in range(2):                           # gamma has no gradient: its guard closes
+            na = grads[a] / np.linalg.norm(grads[a])
+            pdot = (new[a, 0, 0, 0] - old[a, 0, 0, 0]) / pd["dt"]
+            w = math.pi * pd["eps"] / 4 * ph[a] * hl / math.sqrt(ph[a] * ph[3]) * pdot * (na @ nl) * na[d]
+            for cc in range(2):
+                dc = 0.0
+                for cell in (lo, hi):
+                    T = p.T0 + pd["G"] * ((cell[2] + zorig + 0.5) - pd["v"] * step_n * pd["dt"])
+                    m = mu[cc, cell[2], cell[1], cell[0]]
+                    dc += 0.5 * (O.conc(p, 3, cc, m, T) - O.conc(p, a, cc, m, T))
+                expect[cc] += w * dc
+        _, J = O.mu_face(p, old, new, mu, int(lo[0]), int(lo[1]), int(lo[2]), d, n=step_n, zorig=zorig)
+        assert np.abs(J - expect).max() <= 1e-13 * np.abs(expect).max(), (d, J, expect)
+
+
+def test_p20_anisotropic_phi_face_exact_on_linear_fields(pv1):
+    n, c = 9, (4, 4, 4)
+    grads = [np.array([0.010, 0.020, -0.015]), np.array([-0.012, 0.008, 0.011]), np.array([0.004, -0.009, 0.006])]
+    base = [0.30, 0.20, 0.15]
+    phi = _linear_phi(n, grads, base, c)
+    p = _params(pv1, aniso=True, delta_sl=0.05)
+    g4 = grads + [-(grads[0] + grads[1] + grads[2])]
+    for d in range(3):
+        e = np.eye(3, dtype=int)[d]
+        xf = np.array(c) + 0.5 * e
+        pb = np.array([base[a] + grads[a] @ (xf - c) for a in range(3)])
+        pb = np.append(pb, 1.0 - pb.sum())
+        expect = np.zeros(4)
+        for a in range(4):
+            for b in range(4):
+                if a == b:
+                    continue
+                q = pb[a] * g4[b] - pb[b] * g4[a]
+                # j_a = -sum_b g_ab,d(q_ab) phibar_b (O4.5); g from the pinned pair_grad (P8)
+                expect[a] -= O.pair_grad(p, min(a, b), max(a, b), q if a < b else -q)[d] * (1 if a < b else -1) * pb[b]
+        jf = O.phi_face(p, phi, c[0], c[1], c[2], d)
+        assert np.abs(jf - expect).max() <= 1e-13 * np.abs(expect).max(), (d, jf, expect)
+
+
+# --------------------------------------------------------------------------
+# P21 — homogeneity of the cubic gradient energy (reading R3): a_c depends on
+# q/|q| only, so e(s q) = s^2 e(q) and g(s q) = s g(q) for every s > 0, and g
+# goes to 0 continuously as q -> 0 (no under/overflow of |q|^6)
+# --------------------------------------------------------------------------
+def test_p21_gradient_energy_homogeneity(pv1):
+    p = _params(pv1, aniso=True, delta_sl=0.05)
+    rng = np.random.default_rng(21)
+    for _ in range(20):
+        q = rng.normal(0, 1, 3)
+        g1, e1 = O.pair_grad(p, 0, 3, q), O.pair_energy(p, 0, 3, q)
+        for s in [1e-150, 1e-100, 1e-80, 1e-60, 1e-20, 3.7, 1e20, 1e60, 1e100]:
+            gs = O.pair_grad(p, 0, 3, s * q)
+            assert np.all(np.isfinite(gs))
+            assert np.abs(gs - s * g1).max() <= 2e-15 * s * np.abs(g1).max(), s
+            if 1e-150 < s < 1e150:
+                es = O.pair_energy(p, 0, 3, s * q)
+                assert abs(es - s * s * e1) <= 2e-15 * s * s * e1, s
+        for s in [2.0 ** -300, 2.0 ** -40, 2.0 ** 50, 2.0 ** 300]:   # powers of two: bit for bit
+            assert np.array_equal(O.pair_grad(p, 0, 3, s * q), s * g1)
