@@ -9,9 +9,11 @@ PARAMS-v1, synthetic data.  One "step" = one pass of the whole hot path
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-N > 1 is launched by the driver under torch.distributed.run (one rank per
-GPU, NCCL).  Rank 0 prints one JSON line.  --impl reference times the CPU
-oracle (the only reference implementation of this tier) on host cores.
+N > 1 runs one rank per GPU over NCCL: under torch.distributed.run (the
+driver's launch; WORLD_SIZE must equal N), or — started as a plain process —
+bench.py re-launches itself under torch.distributed.run with N ranks.  Rank 0
+prints one JSON line.  --impl reference times the CPU oracle (the only
+reference implementation of this tier) on host cores.
 """
 from __future__ import annotations
 
@@ -33,6 +35,13 @@ CONFIG = "c4"
 # (oracle.count_flops, isotropic), compulsory FP64 bytes.
 BYTES_PHI, BYTES_MU = 80, 96
 PEAK_FP64_DERIVED = 148 * 64 * 2 * 1.965e9 / 1e12   # TFLOP/s: SMs x FP64 FMA/clk x 2 x max clock
+# SURVEY.md §8(d)'s counted FLOP/LUP (a scratch op count of O4/O5 made during
+# the survey), reported beside the oracle's own count
+FLOP_SURVEY = {"phi_iso": 522, "phi_aniso": 1422, "mu": 638}
+FLOP_METHOD = ("oracle/oracle.cpp or_count_flops: + - x / sqrt = 1 each, every face charged once, per-plane "
+               "(T-only) values free, no shortcuts and every anti-trapping guard open (PAPER.md:508-509); "
+               "de-duplicated: S and psi-bar once per cell, only the normal component g_d of a pair gradient "
+               "at a face, the liquid normal once per face")
 
 
 def _env_int(k, d):
@@ -134,32 +143,60 @@ def flops_per_lup(name):
     return d["configs"][name]
 
 
-def cpu_oracle_sample(name: str, steps: int, nz_slab: int = 16):
+def cpu_oracle_sample(name: str, steps: int, nz_slab: int = 16, threads: int | None = None, sweep: str = "step",
+                      nxy: int = 512):
     """Time the CPU oracle (as it stands) on a bounded sample of the workload:
-    the full x-y extent of one GPU's block, nz_slab planes around the
-    solid-liquid front of the config's initial state, stepped as its own domain
-    (uniform per-cell work: the oracle takes no shortcuts).
-    Returns (MLUP/s, cores, sample text)."""
+    an nxy x nxy x nz_slab slab of one GPU's block around the solid-liquid front
+    of the config's initial state, stepped as its own domain (uniform per-cell
+    work: the oracle takes no shortcuts).  sweep = "step" (phi + mu) or "mu"
+    (the mu-sweep alone, the paper's per-core figure is mu-only).
+    threads = OpenMP threads (None: all host cores).
+    Returns (MLUP/s, threads, sample text)."""
     from inputs import gen
     from oracle import oracle as O
     cfg = load_cfg(name)
     pd = gen.load_params("v1")
     lh = cfg["init"]["layer_height"]
-    nx, ny = min(cfg["nx"], 512), min(cfg["ny"], 512)
+    nx, ny = min(cfg["nx"], nxy), min(cfg["ny"], nxy)
     spec = gen.spec_from_config(cfg, cfg["nx"], cfg["ny"])
     nz_slab = min(nz_slab, cfg["nz"])
     z0 = max(0, min(int(lh) - nz_slab // 2, cfg["nz"] - nz_slab))
     phi, mu = gen.generate(spec, cfg["nx"], cfg["ny"], cfg["nz"], box=(0, 0, z0, nx, ny, nz_slab))
     p = O.make_params(pd, layer_height=lh - z0, aniso=cfg.get("aniso", False), delta_sl=cfg.get("delta_sl"))
+    cores = int(threads) if threads else (os.cpu_count() or 1)
+    O.set_threads(cores)
+    if sweep == "mu":
+        phi1 = O.phi_sweep(p, phi, mu, 0, 0)
     t0 = time.perf_counter()
     for s in range(steps):
-        phi, mu = O.step(p, phi, mu, s, 0)
+        if sweep == "mu":
+            mu = O.mu_sweep(p, phi, phi1, mu, 0, 0)
+        else:
+            phi, mu = O.step(p, phi, mu, s, 0)
     dt = time.perf_counter() - t0
+    O.set_threads(None)
     cells = nx * ny * nz_slab
-    cores = _env_int("OMP_NUM_THREADS", os.cpu_count() or 1)
+    what = "mu-sweep(s)" if sweep == "mu" else "oracle step(s)"
     return cells * steps / dt / 1e6, cores, \
-        f"{steps} oracle step(s) of the {nx}x{ny}x{nz_slab} slab z in [{z0},{z0 + nz_slab}) of the " \
-        f"{cfg['name']} state ({cells * steps} LUP, {dt:.1f} s)"
+        f"{steps} {what} of the {nx}x{ny}x{nz_slab} slab z in [{z0},{z0 + nz_slab}) of the " \
+        f"{cfg['name']} state on {cores} thread(s) ({cells * steps} LUP, {dt:.1f} s)"
+
+
+def cpu_baseline(name: str, steps: int, aniso: bool):
+    """The oracle on the box's host cores:
+    all cores and one core, full step and mu-sweep alone; MLUP/s and per core."""
+    nzs = 16 if aniso else 64
+    v, cores, sample = cpu_oracle_sample(name, steps, nz_slab=nzs)
+    v1, _, s1 = cpu_oracle_sample(name, 1, nz_slab=16, threads=1, nxy=256)
+    vm, _, sm = cpu_oracle_sample(name, max(1, steps // 2), nz_slab=nzs, sweep="mu")
+    vm1, _, sm1 = cpu_oracle_sample(name, 1, nz_slab=16, threads=1, sweep="mu", nxy=256)
+    return {"value": round(v, 3), "unit": "MLUP/s", "cores": cores, "per_core": round(v / cores, 3),
+            "cpu": cpu_model(), "kind": "oracle", "sample": sample,
+            "single_core": {"value": round(v1, 3), "sample": s1},
+            "mu_sweep": {"all_cores": round(vm, 3), "per_core": round(vm / cores, 3), "single_core": round(vm1, 3),
+                         "samples": [sm, sm1]},
+            "more": "profiles/r02_cpu_baseline.json (tools/cpu_baseline.py: C1 and C2 100-step runs, "
+                    "median of 3 after warm-up)"}
 
 
 def describe(cfg, grid, blocks, scaling):
@@ -239,23 +276,32 @@ def run_gpu(args):
     # a graph replay has no per-sweep events, so --graph times them after)
     ctx.set_timing(not args.graph)
     l0 = ctx.info().launches
-    barrier()
-    torch.cuda.synchronize()
+    # args.reps windows of exactly args.steps steps, each bracketed by a barrier
+    # and a synchronize; the median window is reported
+    windows = []
     clocks.start()
-    e0.record(stream)
-    ctx.step(args.steps)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
+    for _ in range(max(1, args.reps)):
+        ctx.set_timing(not args.graph)   # resets the per-sweep accumulators
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        ctx.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        inf = ctx.info()
+        windows.append((max_over_ranks(e0.elapsed_time(e1)), inf.ms_phi / max(1, inf.phi_launches),
+                        inf.ms_mu / max(1, inf.mu_launches)))
     clk = clocks.stop()
-    ms = max_over_ranks(e0.elapsed_time(e1))
-    launches = int(ctx.info().launches - l0)
+    launches = int(ctx.info().launches - l0) // max(1, args.reps)
+    order = sorted(range(len(windows)), key=lambda i: windows[i][0])
+    ms, ms_phi, ms_mu = windows[order[len(order) // 2]]
     if args.graph:
         ctx.set_timing(True)
         ctx.step(min(args.steps, 10))
-    inf = ctx.info()
-    ms_phi = inf.ms_phi / max(1, inf.phi_launches)
-    ms_mu = inf.ms_mu / max(1, inf.mu_launches)
+        inf = ctx.info()
+        ms_phi = inf.ms_phi / max(1, inf.phi_launches)
+        ms_mu = inf.ms_mu / max(1, inf.mu_launches)
     ctx.set_timing(False)
     value = cells_local * world * args.steps / (ms / 1e3) / 1e6
 
@@ -290,6 +336,29 @@ def run_gpu(args):
         e2e_job = cells_local * world * args.steps / job_s / 1e6
         del hphi, hmu
 
+    # the no-shortcut, interface-dense measurement ("without
+    # the shortcut optimizations ... the total number of executed floating point
+    # operations per cell can be determined exactly"; the interface scenario,
+    # PAPER.md:424-427): a state with all four phases in every cell (every
+    # anti-trapping guard open on every face) written with pf_write, one timed
+    # step per repetition from that state
+    iface = None
+    if not args.no_interface:
+        from inputs import gen as _gen
+        dphi, dmu = _gen.interface_state_torch(shape, seed=cfg["seed"], device="cuda")
+        reps = []
+        for _ in range(5):
+            ctx.write(dphi, dmu)
+            ctx.set_timing(True)
+            ctx.step(1)
+            inf = ctx.info()
+            reps.append((inf.ms_phi / max(1, inf.phi_launches), inf.ms_mu / max(1, inf.mu_launches)))
+        ctx.set_timing(False)
+        del dphi, dmu
+        torch.cuda.empty_cache()
+        iface = {"phi_ms": max_over_ranks(float(np.median([r[0] for r in reps]))),
+                 "mu_ms": max_over_ranks(float(np.median([r[1] for r in reps])))}
+
     if rank == 0:
         fl = flops_per_lup(args.config)
         peaks = {}
@@ -298,15 +367,28 @@ def run_gpu(args):
         except (OSError, ValueError):
             pass
         hbm = float(peaks.get("hbm_gbs", 6650.0))
+        aniso = bool(cfg.get("aniso"))
+        f_svy = {"phi": FLOP_SURVEY["phi_aniso" if aniso else "phi_iso"], "mu": FLOP_SURVEY["mu"]}
         sweeps = {
             "phi": {"ms": ms_phi, "flop": fl["phi_per_lup"], "bytes": BYTES_PHI},
             "mu": {"ms": ms_mu, "flop": fl["mu_per_lup"], "bytes": BYTES_MU},
         }
-        for s in sweeps.values():
+        for k, s in sweeps.items():
             s["tflops"] = s["flop"] * cells_local / (s["ms"] / 1e3) / 1e12
             s["gbs"] = s["bytes"] * cells_local / (s["ms"] / 1e3) / 1e9
             s["frac_fp64"] = s["tflops"] / PEAK_FP64_DERIVED
             s["frac_hbm"] = s["gbs"] / hbm
+            s["flop_survey"] = f_svy[k]
+            s["frac_fp64_survey"] = f_svy[k] * cells_local / (s["ms"] / 1e3) / 1e12 / PEAK_FP64_DERIVED
+        if iface:
+            for k in ("phi", "mu"):
+                t = iface[f"{k}_ms"] / 1e3
+                iface[f"{k}_frac_fp64"] = sweeps[k]["flop"] * cells_local / t / 1e12 / PEAK_FP64_DERIVED
+                iface[f"{k}_frac_hbm"] = sweeps[k]["bytes"] * cells_local / t / 1e9 / hbm
+                iface[f"{k}_frac_fp64_survey"] = f_svy[k] * cells_local / t / 1e12 / PEAK_FP64_DERIVED
+            iface["state"] = ("inputs/gen.py interface_state_torch: phi = 0.05 + U(0,1) per phase, normalised "
+                              "(all four phases in every cell), mu = U(-0.3, 0.3); one step from it per repetition, "
+                              "median of 5")
         dom = max(sweeps, key=lambda k: sweeps[k]["ms"])
         d = sweeps[dom]
         traffic = None
@@ -316,13 +398,14 @@ def run_gpu(args):
                 traffic = prof.get("dram_bytes_per_launch", {}).get(dom)
         except (OSError, ValueError):
             pass
-        cpu_v, cores, sample = (None, None, "skipped")
+        cpu = {"value": None, "unit": "MLUP/s", "cores": None, "kind": "oracle", "sample": "skipped"}
         if world == 1 and not args.no_cpu:
-            cpu_v, cores, sample = cpu_oracle_sample(args.config, args.cpu_steps,
-                                                     nz_slab=64 if not cfg.get("aniso") else 16)
+            cpu = cpu_baseline(args.config, args.cpu_steps, bool(cfg.get("aniso")))
         line = {
             "metric": "MLUP/s", "value": round(value, 2), "unit": "MLUP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+            "reps": {"n": len(windows), "ms_per_step": [round(w[0] / args.steps, 4) for w in windows],
+                     "reported": "median window"},
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded initial state, PARAMS-v1)",
             "config": {"workload": describe(cfg, (NX, NY, NZ), (px, py, pz), scaling),
@@ -332,17 +415,21 @@ def run_gpu(args):
             "roofline": {"bound": "alu", "kernel": f"{dom}-sweep", "achieved": round(d["tflops"], 3),
                          "peak": round(PEAK_FP64_DERIVED, 2), "unit": "TFLOP/s",
                          "frac": round(d["frac_fp64"], 4), "traffic": traffic,
+                         "flop_per_lup": d["flop"], "flop_method": FLOP_METHOD,
+                         "frac_at_survey_flop": round(d["frac_fp64_survey"], 4),
                          "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md §6); "
                                         "measured DFMA loop 34.2 TFLOP/s",
                          "sweeps": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv)
                                         for kk, vv in s.items()} for k, s in sweeps.items()},
-                         "note": "flop = algorithmic FLOP/LUP counted from the oracle with every term evaluated "
-                                 "(PAPER.md:508-509); the mu-sweep's exact-zero anti-trapping guards skip most "
-                                 "of its FP64 work on bulk planes, so mu is judged by frac_hbm (96 B/LUP)",
+                         "note": "flop = algorithmic FLOP/LUP (flop_method); flop_survey = SURVEY.md §8(d)'s count. "
+                                 "On the C4 state the mu-sweep's exact-zero anti-trapping guards skip most of its "
+                                 "FP64 work (bulk planes), so there mu is judged by frac_hbm (96 B/LUP) and by "
+                                 "mu_interface, the all-guards-open state",
+                         "mu_interface_ms": round(iface["mu_ms"], 4) if iface else None,
+                         "interface": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in iface.items()}
+                         if iface else None,
                          "hbm_peak_gbs": hbm},
-            "cpu_baseline": {"value": round(cpu_v, 3) if cpu_v else None, "unit": "MLUP/s", "cores": cores,
-                             "per_core": round(cpu_v / cores, 3) if cpu_v else None, "cpu": cpu_model(),
-                             "kind": "oracle", "sample": sample},
+            "cpu_baseline": cpu,
             "paper_context": {"mlups_per_core": 4.2, "what": "mu-kernel only (no phi), one SuperMUC Sandy Bridge "
                               "core, SIMD-optimised, Ag-Al-Cu parameters (PAPER.md:526); the paper prints no GPU "
                               "or full-step number", "unit": "MLUP/s/core"},
@@ -363,6 +450,40 @@ def run_gpu(args):
     return 0
 
 
+def relaunch_distributed(n: int) -> int:
+    """Started as a plain process with --gpus N > 1: run the same command as N
+    ranks under torch.distributed.run (one per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench.py: --gpus {n} without a launcher: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def check_world(args) -> int | None:
+    """--gpus N against the launcher's WORLD_SIZE: re-launch when there is no
+    launcher, refuse a mismatch (a run must not label one GPU's number as N's).
+    Returns an exit code to stop with, or None to go on."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None:
+        if args.gpus > 1:
+            if args.impl == "ours":
+                import torch
+                have = torch.cuda.device_count()
+                if have < args.gpus:
+                    print(f"bench.py: --gpus {args.gpus} but {have} GPU(s) visible", file=sys.stderr)
+                    return 2
+            return relaunch_distributed(args.gpus)
+        return None
+    if int(ws) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}: refusing to run", file=sys.stderr)
+        return 2
+    return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -372,6 +493,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-steps", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--reps", type=int, default=3, help="timed windows of --steps steps each; the median is reported")
+    ap.add_argument("--no-interface", action="store_true", help="skip the all-guards-open sweep measurement")
     ap.add_argument("--graph", action="store_true", help="replay each step as a CUDA graph (single rank)")
     ap.add_argument("--grid", type=int, nargs=3, metavar=("NX", "NY", "NZ"),
                     help="global grid overriding the config's (its physics and init recipe kept)")
@@ -379,6 +502,11 @@ def main():
                     help="c4: weak scaling 512^3 per GPU (default, the headline); c5: strong scaling 1024^3, "
                          "anisotropic; c1-c3: the single-GPU parity configs")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    rc = check_world(args)
+    if rc is not None:
+        return rc
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":

@@ -156,8 +156,10 @@ pf_status pf_halo_plan(const pf_grid *g, int32_t field, int64_t *send_counts, in
 /* Validate grid and parameters, select the device, allocate fields and
  * buffers, create the communicator (nranks > 1; collective over all ranks).
  * Errors: PF_ERR_CONFIG (divisibility, gamma not symmetric / non-positive,
- * A(T) <= 0 within the run's temperature range), PF_ERR_ARG, PF_ERR_CUDA,
- * PF_ERR_COMM.  On success *out owns everything. */
+ * A(T) <= 0 over the initial window's temperatures, dt above the explicit-Euler
+ * bound min(dx^2/(6 D_mu), dx^2/(6 D_phi)) of PAPER.md:84-86 — D_mu = D_max
+ * A_max/A_min, D_phi = 2 gamma_max T_max/tau_min, reading R29),
+ * PF_ERR_ARG, PF_ERR_CUDA, PF_ERR_COMM.  On success *out owns everything. */
 pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out);
 
 /* Deterministic, decomposition-independent initial state from `seed` and the
@@ -175,7 +177,11 @@ pf_status pf_set_time(pf_ctx *c, int64_t step, int64_t z_origin);
 /* Advance n explicit steps (Algorithm 1 + window).  Blocking: returns after
  * the last step completed on the device.  Errors: PF_ERR_STATE before
  * pf_init/pf_write, PF_ERR_NUMERICAL with step, global cell and field in
- * pf_last_error when the NaN check trips, PF_ERR_CUDA / PF_ERR_COMM. */
+ * pf_last_error when the NaN check trips, PF_ERR_CUDA / PF_ERR_COMM.
+ * PF_ERR_CONFIG before any work if the temperatures the n steps reach (t up to
+ * (step + n) dt, z over the window incl. up to n origin shifts) make some
+ * A(T) <= 0 or break the dt bound of pf_create; that rejection does not poison
+ * the context (message in pf_last_error). */
 pf_status pf_step(pf_ctx *c, int64_t n);
 
 /* Copy the rank's interior state out (layout above; host or device). */

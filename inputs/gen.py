@@ -96,3 +96,18 @@ def load_params(name: str = "v1") -> dict:
     root = os.path.dirname(_HERE)
     with open(os.path.join(root, "params", f"{name}.json")) as f:
         return json.load(f)
+
+
+def interface_state_torch(shape, seed: int, device="cuda"):
+    """Interface-dense measurement state on the device (torch RNG, seeded):
+    phi = 0.05 + U(0,1) per phase, normalised onto the simplex, so all four
+    phases are present in every cell and every anti-trapping guard is open on
+    every face (the no-shortcut count of PAPER.md:508-509); mu = U(-0.3, 0.3).
+    Input layout only: phi[4, nz, ny, nx], mu[2, nz, ny, nx] float64."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed) * 7919 + 17)
+    phi = torch.rand((4,) + tuple(shape), generator=g, device=device, dtype=torch.float64).add_(0.05)
+    phi /= phi.sum(dim=0, keepdim=True)
+    mu = torch.rand((2,) + tuple(shape), generator=g, device=device, dtype=torch.float64).mul_(0.6).sub_(0.3)
+    return phi, mu

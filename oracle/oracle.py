@@ -83,6 +83,13 @@ def lib():
     return _lib
 
 
+def set_threads(n: int | None):
+    """OpenMP threads of the oracle's z-plane loops (None: all host cores)."""
+    L = lib()
+    L.omp_set_num_threads.argtypes = [ctypes.c_int]
+    L.omp_set_num_threads(int(n) if n else (os.cpu_count() or 1))
+
+
 def make_params(pd: dict, *, layer_height: float | None = None, T0: float | None = None,
                 aniso: bool = False, delta_sl: float | None = None) -> OrParams:
     """Fill OrParams from a params/*.json dict.  T0 = T_eut - G*layer_height

@@ -107,9 +107,38 @@ __device__ __forceinline__ double2 tab2(const double *__restrict__ tab, int base
 // a_c = 1 - delta (3 - 4 Q4/|q|^4) (reading R3); g = 0 at q = 0.
 // Pinned: used inside face fluxes.  Returns g (without the 2 gamma factor
 // folded: full g).
-__device__ __forceinline__ void pair_grad_aniso(double g2, double delta, const double q[3], double out[3]) {
-  const double q2 = RN_FMA(q[2], q[2], RN_FMA(q[1], q[1], RN_MUL(q[0], q[0])));
-  if (q2 == 0.0) { out[0] = out[1] = out[2] = 0.0; return; }
+//
+// g is homogeneous of degree 1 in q (a_c depends on q/|q| only).  The direct
+// formula needs |q|^-4 and Q4 = sum q_d^4, which over- / underflow outside
+// |q| ~ 2^+-250; there (and at q = 0) the slow path evaluates it on q scaled by
+// a power of two into [1, 2) and scales the result back — exact scalings, so it
+// returns the bits the direct formula would give without the range limit.  The
+// range test is one integer compare on |q|^2's exponent (2^-400 <= |q|^2 <
+// 2^400; 0, subnormals, inf and NaN fall outside).
+__device__ __forceinline__ bool q2_extreme(double q2) {
+  return (unsigned)(__double2hiint(q2) - 0x26F00000) >= 0x32000000u;
+}
+__device__ __forceinline__ double pow2_d(int e) {   // 2^e, -1022 <= e <= 1023
+  return __hiloint2double((1023 + e) << 20, 0);
+}
+// scale q (!= 0) in place by 2^-s so that max |q_d| is in [1, 2); returns s
+__device__ __forceinline__ int pow2_normalise(double q[3]) {
+  int s = 0;
+  int m = max(__double2hiint(q[0]) & 0x7fffffff, max(__double2hiint(q[1]) & 0x7fffffff, __double2hiint(q[2]) & 0x7fffffff));
+  if ((m >> 20) == 0) {   // largest component subnormal: lift by 2^600 first (exact)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) q[d] *= pow2_d(600);
+    s = -600;
+    m = max(__double2hiint(q[0]) & 0x7fffffff, max(__double2hiint(q[1]) & 0x7fffffff, __double2hiint(q[2]) & 0x7fffffff));
+  }
+  const int ex = (m >> 20) - 1023;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) q[d] *= pow2_d(-ex);
+  return s + ex;
+}
+__device__ __forceinline__ bool is_zero3(const double q[3]) { return q[0] == 0.0 && q[1] == 0.0 && q[2] == 0.0; }
+__device__ __forceinline__ void pair_grad_aniso_core(double g2, double delta, const double q[3], double q2,
+                                                     double out[3]) {
   double s2[3], s4 = 0.0;
 #pragma unroll
   for (int d = 0; d < 3; ++d) { s2[d] = RN_MUL(q[d], q[d]); }
@@ -126,12 +155,26 @@ __device__ __forceinline__ void pair_grad_aniso(double g2, double delta, const d
     out[d] = RN_MUL(RN_MUL(g2, ac), RN_FMA(d16, t, RN_MUL(ac, q[d])));
   }
 }
+__device__ __forceinline__ double q2_of(const double q[3]) {
+  return RN_FMA(q[2], q[2], RN_FMA(q[1], q[1], RN_MUL(q[0], q[0])));
+}
+__device__ __forceinline__ void pair_grad_aniso(double g2, double delta, const double q[3], double out[3]) {
+  const double q2 = q2_of(q);
+  if (q2_extreme(q2)) {
+    if (is_zero3(q)) { out[0] = out[1] = out[2] = 0.0; return; }
+    double u[3] = {q[0], q[1], q[2]};
+    const int s = pow2_normalise(u);
+    pair_grad_aniso_core(g2, delta, u, q2_of(u), out);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) out[d] *= pow2_d(s);
+    return;
+  }
+  pair_grad_aniso_core(g2, delta, q, q2, out);
+}
 
 // Component d alone of pair_grad_aniso (the face flux needs only the normal
 // component): the same pinned operations, so bitwise the same value.
-__device__ __forceinline__ double pair_grad_aniso_d(double g2, double delta, const double q[3], int d) {
-  const double q2 = RN_FMA(q[2], q[2], RN_FMA(q[1], q[1], RN_MUL(q[0], q[0])));
-  if (q2 == 0.0) return 0.0;
+__device__ __forceinline__ double pair_grad_aniso_core_d(double g2, double delta, const double q[3], double q2, int d) {
   double s2[3];
 #pragma unroll
   for (int e = 0; e < 3; ++e) s2[e] = RN_MUL(q[e], q[e]);
@@ -143,6 +186,16 @@ __device__ __forceinline__ double pair_grad_aniso_d(double g2, double delta, con
   const double d16 = RN_MUL(16.0, delta);
   const double t = RN_MUL(RN_FMA(s2[d], q[d], -RN_MUL(RN_MUL(s4, r2), q[d])), r2);
   return RN_MUL(RN_MUL(g2, ac), RN_FMA(d16, t, RN_MUL(ac, q[d])));
+}
+__device__ __forceinline__ double pair_grad_aniso_d(double g2, double delta, const double q[3], int d) {
+  const double q2 = q2_of(q);
+  if (q2_extreme(q2)) {
+    if (is_zero3(q)) return 0.0;
+    double u[3] = {q[0], q[1], q[2]};
+    const int s = pow2_normalise(u);
+    return pair_grad_aniso_core_d(g2, delta, u, q2_of(u), d) * pow2_d(s);
+  }
+  return pair_grad_aniso_core_d(g2, delta, q, q2, d);
 }
 
 // Face flux j_a (component d) of the phi-sweep between cells lo and hi = lo+e_d

@@ -235,7 +235,9 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
       }
       return __all_sync(0xffffffffu, mine || !active) != 0;
     };
-    bool skip = ANISO ? false : bulk_warp();
+    // the vote reads slot(k-1), which stage(k+3) refills right after B(k): it
+    // is taken before the barrier in both kernels
+    const bool skip = bulk_warp();
     // isotropic: the cell terms that need no face flux (phi_cell_rhs0, on the
     // raw centre differences) are formed before the barrier, where the tile
     // values are still at hand; the anisotropic kernel has no registers to
@@ -255,7 +257,6 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
       for (int a = 0; a < NPH; ++a) q[a] = r0[a] - c * dpart[a];
     }
     __syncthreads();  // B: faces of plane k complete
-    if (ANISO) skip = bulk_warp();
     if (active && skip) {
       const int64_t o = (int64_t)k * b.plane + colo;
 #pragma unroll

@@ -91,6 +91,7 @@ struct pf_ctx {
   int64_t step = 0, zorig = 0, shifts = 0, last_front = -1, next_check = 0;
   int slack = 0;
   bool initialized = false;
+  bool plans_woff0 = false;  // the halo plans are current and were built with every woff = 0
   pf_status status = PF_OK;
   std::string err;
   // timing
@@ -426,6 +427,8 @@ pf_status build_plans(pf_ctx *c) {
       CKS(upload_ops(c, unpack, &pl.d_unpack, &pl.ctas_unpack));
     }
   }
+  c->plans_woff0 = true;
+  for (const auto &b : c->blocks) if (b.woff != 0) c->plans_woff0 = false;
   return PF_OK;
 }
 
@@ -902,6 +905,52 @@ void ckpt_convert(pf_ctx *c, const CkptChunk &ch, float *d, bool to_fields) {
   launch_cvt32(c->stream, f, b.nx, b.ny, ch.nzc, b.pitch, b.plane, d, b.nx, b.ny, 0, 0, 0, to_fields);
 }
 
+// Explicit Euler is stable only for
+// dt <= min(dx^2 / (6 D_mu), dx^2 / (6 D_phi)) (reading R29):
+//   D_mu  = max_{a,c} D_c^a * max A / min A  (M/chi = sum phi D/(2A) /
+//           sum h/(2A) <= D_max A_max/A_min on the simplex, 7-point Laplacian);
+//   D_phi = 2 gamma_max T_max / tau_min  (the face flux of phase a carries
+//           2 sum_b gamma_ab phibar_b^2 grad phi_a, and Eq. (1) divides eps T
+//           by tau eps).
+// Checked with A(T) > 0 (the parabolas' curvature, reading R7) over the
+// temperatures T0 + G (z dx - v t) at the corners of z in [zlo, zhi] (plane
+// indices incl. window origin), t in [tlo, thi].
+bool t_range_ok(const pf_params &p, double zlo, double zhi, double tlo, double thi, char *why, size_t nwhy) {
+  double Tmin = 1e300, Tmax = -1e300;
+  for (double z : {zlo, zhi})
+    for (double t : {tlo, thi}) {
+      const double T = p.T0 + p.G * ((z + 0.5) * p.dx - p.v * t);
+      Tmin = std::min(Tmin, T);
+      Tmax = std::max(Tmax, T);
+    }
+  double Amin = 1e300, Amax = 0.0, Dmax = 0.0, gmax = 0.0, taumin = 1e300;
+  for (double T : {Tmin, Tmax})
+    for (int a = 0; a < 4; ++a)
+      for (int q = 0; q < 2; ++q) {
+        const double A = p.A0[a][q] + p.A1[a][q] * (T - p.T_eut);
+        if (!(A > 0)) {
+          snprintf(why, nwhy, "A[%d][%d](T=%g) <= 0 (temperatures %g..%g over z %g..%g, t %g..%g)", a, q, T, Tmin,
+                   Tmax, zlo, zhi, tlo, thi);
+          return false;
+        }
+        Amin = std::min(Amin, A);
+        Amax = std::max(Amax, A);
+      }
+  for (int a = 0; a < 4; ++a) {
+    taumin = std::min(taumin, p.tau[a]);
+    for (int q = 0; q < 2; ++q) Dmax = std::max(Dmax, p.D[a][q]);
+    for (int b = 0; b < 4; ++b) if (a != b) gmax = std::max(gmax, p.gamma[a][b]);
+  }
+  const double Dmu = Dmax * Amax / Amin, Dphi = 2.0 * gmax * std::max(Tmax, 0.0) / taumin;
+  const double lim = p.dx * p.dx / (6.0 * std::max(Dmu, Dphi));
+  if (!(p.dt <= lim)) {
+    snprintf(why, nwhy, "dt = %g above the explicit-Euler bound %g (D_mu %g, D_phi %g; DESIGN.md R29)", p.dt, lim,
+             Dmu, Dphi);
+    return false;
+  }
+  return true;
+}
+
 pf_status validate(const pf_grid *g, const pf_params *p) {
   pf_ctx *c = nullptr;
   const int64_t n[3] = {g->nx, g->ny, g->nz};
@@ -926,14 +975,15 @@ pf_status validate(const pf_grid *g, const pf_params *p) {
   if (!(p->dt > 0) || !(p->dx > 0) || !(p->eps > 0)) return fail(c, PF_ERR_CONFIG, "dt, dx, eps must be > 0");
   for (int a = 0; a < 4; ++a)
     if (!(p->tau[a] > 0)) return fail(c, PF_ERR_CONFIG, "tau[%d] must be > 0", a);
-  // A(T) > 0 over the initial window (z in [-1, NZ+1]) and 10x that span
-  const double Tlo = p->T0 + std::min(0.0, p->G) * (double)(g->nz + 2) * p->dx * 10 - std::fabs(p->G) * p->dx;
-  const double Thi = p->T0 + std::max(0.0, p->G) * (double)(g->nz + 2) * p->dx * 10 + std::fabs(p->G) * p->dx;
-  for (double T : {Tlo, Thi, p->T0})
-    for (int a = 0; a < 4; ++a)
-      for (int q = 0; q < 2; ++q)
-        if (!(p->A0[a][q] + p->A1[a][q] * (T - p->T_eut) > 0))
-          return fail(c, PF_ERR_CONFIG, "A[%d][%d](T=%g) <= 0", a, q, T);
+  // A(T) > 0 and the explicit-Euler step bound over the initial window's
+  // temperatures (z in [-1, NZ+1], t = 0); pf_step re-checks both over the
+  // temperatures the requested steps reach (the isotherm's v t drift, the
+  // window's origin)
+  {
+    char why[256];
+    if (!t_range_ok(*p, -1.0, (double)g->nz + 1.0, 0.0, 0.0, why, sizeof(why)))
+      return fail(c, PF_ERR_CONFIG, "%s", why);
+  }
   if (p->window && !(p->window_frac > 0 && p->window_frac <= 1)) return fail(c, PF_ERR_CONFIG, "window_frac");
   if (p->overlap < 0 || p->overlap > 3) return fail(c, PF_ERR_CONFIG, "overlap must be 0..3");
   return PF_OK;
@@ -1176,9 +1226,12 @@ pf_status pf_init(pf_ctx *c, uint64_t seed) {
 pf_status pf_write(pf_ctx *c, const double *phi, const double *mu) {
   CKS(check_state(c, false));
   if (!phi || !mu) return fail(c, PF_ERR_ARG, "NULL state pointer");
-  for (auto &b : c->blocks) b.woff = 0;
+  // the plans are rebuilt only if a window shift moved a block's ring offset
+  // (pf_step_io's multi-block fallback writes every step)
+  bool fresh = c->plans_woff0;
+  for (auto &b : c->blocks) { fresh = fresh && b.woff == 0; b.woff = 0; }
   c->cur = 0;
-  CKS(build_plans(c));
+  if (!fresh) CKS(build_plans(c));
   CKS(move_state(c, const_cast<double *>(phi), const_cast<double *>(mu), true));
   CKS(fill_all_ghosts(c));
   CK(cudaStreamSynchronize(c->stream));
@@ -1283,6 +1336,16 @@ pf_status capture_step(pf_ctx *c) {
 pf_status pf_step(pf_ctx *c, int64_t n) {
   CKS(check_state(c, true));
   if (n < 0) return fail(c, PF_ERR_ARG, "negative step count");
+  {  // the temperatures these n steps reach: the isotherm's drift over t, and
+     // with the window one origin shift per step at most (reading R16)
+    char why[256];
+    const double z0 = (double)c->zorig - 1.0;
+    const double z1 = (double)(c->zorig + (c->p.window ? n : 0) + c->g.nz) + 1.0;
+    if (!t_range_ok(c->p, z0, z1, (double)c->step * c->p.dt, (double)(c->step + n) * c->p.dt, why, sizeof(why))) {
+      c->err = std::string("pf_step(") + std::to_string((long long)n) + "): " + why;
+      return PF_ERR_CONFIG;   // nothing ran: the context stays usable (no poisoning)
+    }
+  }
   // CUDA graphs (pf_params.graph = 1) for single-rank runs without per-sweep
   // timing: one launch per step instead of five-plus — same results, bit for bit
   const bool use_graph = !c->timing && c->g.nranks == 1 && c->p.graph && n > 0;

@@ -93,7 +93,7 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 // z-chunk length.  Every CTA of a sweep does nearly the same work, so the grid
 // runs in waves of (SMs x resident CTAs per SM); a ragged last wave idles the
 // rest of the GPU (2048 CTAs on 592 slots: 3.46 waves take 4).  The chunk is
-// halved (down to 16 planes; a chunk re-stages one plane above and below)
+// halved (while it is longer than 16 planes, so a chunk keeps >= 9 planes; a chunk re-stages one plane above and below)
 // until the grid spans at least min_waves waves, or (fill_ok) fills its last
 // wave to >= 97 % from at least one full wave.  Measured (512^3, tools/ab_*): the
 // phi-sweep is fastest at ~28 waves (64-plane chunks: 3.93 ms vs 4.09 ms

@@ -181,13 +181,21 @@ def halo_plan(nx, ny, nz, px, py, pz, rank, nranks, field):
     return list(snd), list(rcv)
 
 
-def _ptr(x):
-    """Raw pointer of a numpy array or a torch tensor (host or device)."""
+def _ptr(x, nelem=None):
+    """Raw pointer of a numpy array or a torch tensor (host or device).  Raises
+    ValueError unless it is contiguous float64 and, when nelem is given, holds
+    exactly nelem elements (the C ABI reads / writes that many)."""
     if isinstance(x, np.ndarray):
-        assert x.dtype == np.float64 and x.flags.c_contiguous
-        return x.ctypes.data
-    assert str(x.dtype) == "torch.float64" and x.is_contiguous()
-    return x.data_ptr()
+        if x.dtype != np.float64 or not x.flags.c_contiguous:
+            raise ValueError("expected a C-contiguous float64 array")
+        n, p = x.size, x.ctypes.data
+    else:
+        if str(getattr(x, "dtype", "")) != "torch.float64" or not x.is_contiguous():
+            raise ValueError("expected a contiguous torch.float64 tensor")
+        n, p = x.numel(), x.data_ptr()
+    if nelem is not None and n != nelem:
+        raise ValueError(f"buffer holds {n} doubles, the context's box needs {nelem}")
+    return p
 
 
 class Context:
@@ -209,6 +217,12 @@ class Context:
         inf = self.info()
         self.shape = (int(inf.nz_l), int(inf.ny_l), int(inf.nx_l))
 
+    def _phi_ptr(self, x):
+        return _ptr(x, 4 * self.shape[0] * self.shape[1] * self.shape[2])
+
+    def _mu_ptr(self, x):
+        return _ptr(x, 2 * self.shape[0] * self.shape[1] * self.shape[2])
+
     def _check(self, st):
         if st != PF_OK:
             raise PfError(st, lib().pf_last_error(self._c).decode())
@@ -217,7 +231,7 @@ class Context:
         self._check(lib().pf_init(self._c, seed))
 
     def write(self, phi, mu):
-        self._check(lib().pf_write(self._c, _ptr(phi), _ptr(mu)))
+        self._check(lib().pf_write(self._c, self._phi_ptr(phi), self._mu_ptr(mu)))
 
     def set_time(self, step: int, z_origin: int = 0):
         self._check(lib().pf_set_time(self._c, step, z_origin))
@@ -229,7 +243,7 @@ class Context:
         if phi is None:
             phi = np.empty((4,) + self.shape)
             mu = np.empty((2,) + self.shape)
-        self._check(lib().pf_read(self._c, _ptr(phi), _ptr(mu)))
+        self._check(lib().pf_read(self._c, self._phi_ptr(phi), self._mu_ptr(mu)))
         return phi, mu
 
     def step_io(self, phi_in, mu_in, phi_out=None, mu_out=None):
@@ -238,7 +252,8 @@ class Context:
         if phi_out is None:
             phi_out = np.empty((4,) + self.shape)
             mu_out = np.empty((2,) + self.shape)
-        self._check(lib().pf_step_io(self._c, _ptr(phi_in), _ptr(mu_in), _ptr(phi_out), _ptr(mu_out)))
+        self._check(lib().pf_step_io(self._c, self._phi_ptr(phi_in), self._mu_ptr(mu_in), self._phi_ptr(phi_out),
+                                     self._mu_ptr(mu_out)))
         return phi_out, mu_out
 
     def save(self, path):

@@ -90,3 +90,29 @@ def test_create_validates_before_the_device():
     with pytest.raises(pf.PfError) as e:
         pf.Context(16, 16, 16, prm)
     assert e.value.status == pf.PF_ERR_CONFIG and "not symmetric" in str(e.value)
+
+
+def test_create_rejects_unstable_dt_and_nonpositive_A():
+    # the explicit-Euler bound (reading R29) and
+    # A(T) > 0 over the initial window (reading R7) — before the device
+    import pytest
+    from paper_1506_01684_b200 import pf
+    from inputs import gen
+    cfg = gen.load_config("c1")
+    pd = gen.load_params("v1")
+    # PARAMS-v1: D_mu = 1 * 1.0/0.5 = 2, D_phi = 2 * 1 * T_max / 1 ~ 2: bound ~ 1/12
+    for dt, ok in [(0.03, True), (0.08, True), (0.09, False), (0.5, False)]:
+        prm = pf.make_params(dict(pd, dt=dt), cfg)
+        if ok:
+            try:
+                pf.Context(8, 8, 8, prm)
+            except pf.PfError as e:   # no GPU here: validation passed, the device step failed
+                assert e.status == pf.PF_ERR_CUDA, str(e)
+        else:
+            with pytest.raises(pf.PfError) as e:
+                pf.Context(8, 8, 8, prm)
+            assert e.value.status == pf.PF_ERR_CONFIG and "explicit-Euler bound" in str(e.value), str(e.value)
+    prm = pf.make_params(dict(pd, G=0.5), cfg)        # T over the window reaches A^l(T) <= 0
+    with pytest.raises(pf.PfError) as e:
+        pf.Context(8, 8, 8, prm)
+    assert e.value.status == pf.PF_ERR_CONFIG and "<= 0" in str(e.value), str(e.value)
