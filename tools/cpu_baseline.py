@@ -5,7 +5,8 @@ alone (the paper's 4.2 MLUP/s/core is its SIMD mu-kernel on one SuperMUC
 core).  Median of 3 timed repetitions after warm-up steps.
 The oracle is run as it stands (not tuned for this).
 
-usage: python tools/cpu_baseline.py [--out profiles/r02_cpu_baseline.json] [--quick]
+usage: python tools/cpu_baseline.py [--out gpurun_out/cpu_baseline.json] [--quick]
+(the committed copy is profiles/r02_cpu_baseline.json)
 """
 import argparse
 import json
@@ -64,7 +65,7 @@ def case(label, name, steps, threads, reps, warm, sweep="step", box=None):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_cpu_baseline.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "cpu_baseline.json"))
     ap.add_argument("--quick", action="store_true")
     a = ap.parse_args()
     nc = os.cpu_count() or 1
