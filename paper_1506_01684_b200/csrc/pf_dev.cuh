@@ -16,6 +16,11 @@
 
 namespace pf {
 
+#define RN_ADD __dadd_rn
+#define RN_SUB __dsub_rn
+#define RN_MUL __dmul_rn
+#define RN_FMA __fma_rn
+
 constexpr int NPH = 4;   // phases alpha, beta, gamma, liquid
 constexpr int NMU = 2;   // independent chemical potentials (K-1)
 constexpr int LIQ = 3;
@@ -30,7 +35,10 @@ __host__ __device__ constexpr int pair_of(int a, int b) {
 
 // Per-step constants (kernel argument, lives in the constant bank).
 struct KParams {
-  double dt, inv_dt, inv_dx, inv_2dx, half_inv_dt;
+  double dt, inv_dt, inv_dx, inv_2dx;
+  double pad0_;            // the round-1 layout (a fifth scalar here): with the arrays
+                           // at other offsets the phi-sweep needs 4 more registers and
+                           // spills (measured; -2 % phi time with this layout)
   double dt_taueps[NPH];   // dt / (tau_a eps)
   double g2[6];            // 2 gamma_ab per pair
   double g2c[6];           // 2 gamma_ab / (2 dx)^2 per pair: isotropic Gram of raw centre differences
@@ -39,7 +47,7 @@ struct KParams {
   double delta[6];         // cubic anisotropy per pair
   double g3[NPH];          // triple coefficient of the triple excluding x
   double mch[NPH][NMU];    // m_a,c: the (T-independent) slope of c-hat, O5.5
-  double pi_eps_4;         // pi eps / 4
+  double pi_eps_16dt;      // pi eps / (16 dt): the anti-trapping weight on face sums (mu_face_t)
   double Gv;               // G v = -dT/dt
   int aniso;
   int shortcuts;           // region shortcuts (NEXT-1): skip the phi update of bulk warps
@@ -56,6 +64,18 @@ __device__ __forceinline__ double rcp_nr(double s) {
   r = __fma_rn(r, e, r);
   e = __fma_rn(-s, r, 1.0);
   return __fma_rn(r, e, r);
+}
+
+// 1/sqrt(x) for x in [2^-1000, 2^1000]: the hardware approximation refined by
+// two Newton steps r += r (1 - x r^2) / 2 (pinned; a few ulp, not correctly
+// rounded) — the library rsqrt's special-case handling is 17 instructions.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = RN_FMA(-RN_MUL(x, r), r, 1.0);
+  r = RN_FMA(RN_MUL(0.5, r), e, r);
+  e = RN_FMA(-RN_MUL(x, r), r, 1.0);
+  return RN_FMA(RN_MUL(0.5, r), e, r);
 }
 
 // A cell whose phase vector is a simplex vertex (one component exactly 1, the
@@ -86,7 +106,8 @@ enum {
   T_B = 44,       // + a         L (T - T_eut) / T_eut
   T_DI2A = 48,    // 1/(2A^l) - 1/(2A^a), solids a < 3
   T_DCHAT = 54,   // chat^l - chat^a,     solids a < 3
-  TAB = 60        // multiple of 4 doubles (32 B): rows stay aligned
+  T_DCHAT2 = 60,  // 2 (chat^l - chat^a): the x/y-face sum of (c^l - c^a) (mu_face_t)
+  TAB = 68        // multiple of 4 doubles (32 B): rows stay aligned
 };
 static_assert(TAB % 4 == 0, "table row alignment");
 // the (c = 0, 1) pair of phase a of a per-(phase, component) table entry
@@ -94,10 +115,6 @@ __device__ __forceinline__ double2 tab2(const double *__restrict__ tab, int base
   return *reinterpret_cast<const double2 *>(tab + base + 2 * a);
 }
 
-#define RN_ADD __dadd_rn
-#define RN_SUB __dsub_rn
-#define RN_MUL __dmul_rn
-#define RN_FMA __fma_rn
 
 // ---------------------------------------------------------------------------
 // phi-sweep
@@ -252,6 +269,19 @@ __device__ __forceinline__ void phi_face(const KParams &kp, const double plo[NPH
     }
   }
 }
+
+// x == +-0 as an integer test on the bits (a double compare is an FP64-pipe
+// instruction); false for NaN, like x == 0.0
+__device__ __forceinline__ bool is_zero_bits(double x) { return (__double_as_longlong(x) << 1) == 0ll; }
+// |x| outside [2^-e, 2^e) or zero / subnormal / inf / NaN, from the exponent bits
+__device__ __forceinline__ bool exp_outside(double x, int e) {
+  const int ex = (__double2hiint(x) >> 20) & 0x7ff;   // biased exponent
+  return (unsigned)(ex - (1023 - e)) >= (unsigned)(2 * e);
+}
+
+// Raw centre difference hi - lo (the mu-sweep's anti-trapping gradients, which
+// are scale-free), pinned.
+__device__ __forceinline__ double cdiff(double lo, double hi) { return RN_SUB(hi, lo); }
 
 // Centre gradient (hi - lo) / (2 dx), pinned.
 __device__ __forceinline__ double cgrad(const KParams &kp, double lo, double hi) {
@@ -432,10 +462,11 @@ __device__ __forceinline__ void phi_cell_project(const KParams &kp, const double
 struct MuQ {
   double pn[NPH];     // phi^{n+1}
   double dp[NPH];     // phi^{n+1} - phi^n
-  double gn[NPH][3];  // centre gradient of phi^{n+1} (tangential parts used)
+  double gn[NPH][3];  // raw centre differences phi^{n+1}(c+e) - phi^{n+1}(c-e) (tangential parts used)
   double M[NMU];      // sum_a phi^n_a D/(2A)          (R11)
   double dcl[3][NMU]; // c^l - c^a for the solids a   (R10)
   double mu[NMU];
+  const double *tab;  // the cell's plane table row
 };
 
 // c^l - c^a = mu (1/(2A^l) - 1/(2A^a)) + (chat^l - chat^a) at the plane's T
@@ -458,6 +489,7 @@ __device__ __forceinline__ void mob2(const double *__restrict__ tab, const doubl
 
 __device__ __forceinline__ void mu_cell_q(const double *__restrict__ tab, const double po[NPH],
                                           const double pn[NPH], const double mu[NMU], MuQ &q) {
+  q.tab = tab;
 #pragma unroll
   for (int a = 0; a < NPH; ++a) { q.pn[a] = pn[a]; q.dp[a] = RN_SUB(pn[a], po[a]); }
   mob2(tab, po, q.M);
@@ -471,14 +503,21 @@ __device__ __forceinline__ void mu_cell_q(const double *__restrict__ tab, const 
 
 // (M grad mu - J_at)_c at the face (lo, hi = lo + e_d) — oracle mu_face.
 // One pinned implementation for every operand source: QL / QH are accessors
-// (registers: MuQAcc; shared-memory tiles: see pf_mu.cu) with
-//   pn(a), dp(a) (a < 3), gt(a, e) (centre gradient of phi^{n+1}, e != d),
-//   M(c), mu(c), dcl(a, c).
+// (registers: MuQAcc; shared-memory tiles and records: see pf_mu.cu) with
+//   pn(a), dp(a) (a < 3), gt(a, e) (RAW centre difference of phi^{n+1},
+//   phi(c+e) - phi(c-e), e != d), M(c), mu(c), dcl(a, c).
 // Guards are exact-zero tests (reading R10).  The anti-trapping weight
-//   (pi eps/4) phi_a h_l / sqrt(phi_a phi_l) * dphi_a/dt * (n_a . n_l) * n_a,d
-// is evaluated as (pi eps/4) pb_a h_l pd (g_a . g_l) g_a,d / sqrt(pal |g_l|^2 |g_a|^4)
-// — one FP64 rsqrt per solid instead of three (algebraically identical; a
-// guarded fallback keeps it finite when the product leaves the normal range).
+//   (pi eps/4) phibar_a h_l / sqrt(phibar_a phibar_l) * dphi_a/dt * (n_a . n_l) * n_a,d
+// is homogeneous of degree 0 in phibar and in each gradient vector, so it is
+// evaluated on face SUMS s = lo + hi (= 2 phibar), sum of the dphi (= 2 dt
+// dphi/dt) and gradients scaled by 4 dx (normal 4 (hi - lo), tangential the
+// sum of the two raw centre differences): no 1/2, 1/dx or 1/dt per operand,
+// the constants folded into pi eps / (16 dt) (the (c^l - c^a) sum carries the
+// last 1/2):
+//   w = (pi eps / 16 dt) s_a h_l pd (g_a . g_l) g_a,d / sqrt(s_a s_l |g_l|^2 |g_a|^4)
+// — one FP64 rsqrt per solid (a guarded factorised fallback keeps it finite
+// when the product leaves the normal range).  Equal to the oracle's literal
+// form up to rounding.
 // Diffusive part M grad mu of a face (arithmetic mean of the cell mobilities,
 // reading R11), pinned: the value every face starts from.
 __device__ __forceinline__ double mu_flux_diff(const KParams &kp, double Mlo, double Mhi, double mlo, double mhi) {
@@ -486,48 +525,100 @@ __device__ __forceinline__ double mu_flux_diff(const KParams &kp, double Mlo, do
 }
 
 // DIFF = false: the anti-trapping part -J alone (Algorithm 2's mu-sweep-neighbor).
-template <bool DIFF = true, class QL, class QH>
+// ROLL: the three solids in a loop that is not unrolled (a third of the code
+// and of the live temporaries; only for accessors whose operands are in
+// shared memory — an operand array in registers indexed by a run-time solid
+// would be put in local memory)
+template <bool DIFF = true, bool ROLL = false, class QL, class QH>
 __device__ __forceinline__ void mu_face_t(const KParams &kp, const QL &lo, const QH &hi, int d, double out[NMU]) {
 #pragma unroll
   for (int c = 0; c < NMU; ++c) out[c] = DIFF ? mu_flux_diff(kp, lo.M(c), hi.M(c), lo.mu(c), hi.mu(c)) : 0.0;
-  const double pbl = RN_MUL(0.5, RN_ADD(lo.pn(LIQ), hi.pn(LIQ)));
-  if (pbl == 0.0) return;                   // no liquid: J = 0 (bulk solid exits here)
-  double gfl[3];
+#ifndef PF_MU_RCPNR
+#define PF_MU_RCPNR 1
+#endif
+#ifndef PF_MU_INTZ
+#define PF_MU_INTZ 1
+#endif
+#ifndef PF_MU_HOIST
+#define PF_MU_HOIST 1
+#endif
+#if PF_MU_INTZ
+#define PF_ZERO(x) is_zero_bits(x)
+#else
+#define PF_ZERO(x) ((x) == 0.0)
+#endif
+  const double sl = RN_ADD(lo.pn(LIQ), hi.pn(LIQ));
+  if (PF_ZERO(sl)) return;                  // no liquid: J = 0 (bulk solid exits here)
+  // gradient components in the order (normal d, tangential d+1, d+2) — scalars,
+  // never an array indexed by the run-time d (that would live in local memory)
+  const int e1 = d == 2 ? 0 : d + 1, e2 = d == 0 ? 2 : d - 1;
+  const double ln = RN_MUL(4.0, RN_SUB(hi.pn(LIQ), lo.pn(LIQ)));
+  const double l1 = RN_ADD(lo.gt(LIQ, e1), hi.gt(LIQ, e1)), l2 = RN_ADD(lo.gt(LIQ, e2), hi.gt(LIQ, e2));
+  const double gl2 = RN_FMA(l2, l2, RN_FMA(l1, l1, RN_MUL(ln, ln)));
+  if (PF_ZERO(gl2)) return;                 // flat liquid: J = 0
+  double S = RN_MUL(sl, sl);   // = sum_b s_b^2 with the liquid term first
+  {
+    double sa[3];
 #pragma unroll
-  for (int e = 0; e < 3; ++e)
-    gfl[e] = (e == d) ? RN_MUL(RN_SUB(hi.pn(LIQ), lo.pn(LIQ)), kp.inv_dx)
-                      : RN_MUL(0.5, RN_ADD(lo.gt(LIQ, e), hi.gt(LIQ, e)));
-  const double gl2 = RN_FMA(gfl[2], gfl[2], RN_FMA(gfl[1], gfl[1], RN_MUL(gfl[0], gfl[0])));
-  if (gl2 == 0.0) return;                   // flat liquid: J = 0
-  double pb[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) pb[a] = RN_MUL(0.5, RN_ADD(lo.pn(a), hi.pn(a)));
-  const double S = RN_FMA(pbl, pbl, RN_FMA(pb[2], pb[2], RN_FMA(pb[1], pb[1], RN_MUL(pb[0], pb[0]))));
-  const double hl = RN_MUL(RN_MUL(pbl, pbl), __drcp_rn(S));
+    for (int a = 0; a < 3; ++a) sa[a] = RN_ADD(lo.pn(a), hi.pn(a));
+    S = RN_FMA(sa[2], sa[2], RN_FMA(sa[1], sa[1], RN_FMA(sa[0], sa[0], S)));
+  }
+#if PF_MU_RCPNR
+  const double rS = exp_outside(S, 1000) ? __drcp_rn(S) : rcp_nr(S);   // rcp.approx flushes subnormals
+#else
+  const double rS = __drcp_rn(S);
+#endif
+  // (pi eps / 16 dt) h_l
+  const double khl = RN_MUL(kp.pi_eps_16dt, RN_MUL(RN_MUL(sl, sl), rS));
+  // x / y faces: both cells share the plane's table row, so the (c^l - c^a)
+  // sum is (mu_lo + mu_hi) (1/2A^l - 1/2A^a) + 2 (chat^l - chat^a); a z face's
+  // cells each use their own plane's row
+#if PF_MU_HOIST
+  const double ms0 = RN_ADD(lo.mu(0), hi.mu(0)), ms1 = RN_ADD(lo.mu(1), hi.mu(1));
+#endif
   double J0 = 0.0, J1 = 0.0;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const double pal = RN_MUL(pb[a], pbl);
-    const double pd = RN_MUL(RN_ADD(lo.dp(a), hi.dp(a)), kp.half_inv_dt);
-    double gfa[3];
-#pragma unroll
-    for (int e = 0; e < 3; ++e)
-      gfa[e] = (e == d) ? RN_MUL(RN_SUB(hi.pn(a), lo.pn(a)), kp.inv_dx)
-                        : RN_MUL(0.5, RN_ADD(lo.gt(a, e), hi.gt(a, e)));
-    const double ga2 = RN_FMA(gfa[2], gfa[2], RN_FMA(gfa[1], gfa[1], RN_MUL(gfa[0], gfa[0])));
-    if (pal == 0.0 || ga2 == 0.0 || pd == 0.0) continue;
-    const double dot = RN_FMA(gfa[2], gfl[2], RN_FMA(gfa[1], gfl[1], RN_MUL(gfa[0], gfl[0])));
+  auto solid = [&](int a) {
+    const double saa = RN_ADD(lo.pn(a), hi.pn(a));
+    const double pal = RN_MUL(saa, sl);
+    const double pd = RN_ADD(lo.dp(a), hi.dp(a));
+    const double gn = RN_MUL(4.0, RN_SUB(hi.pn(a), lo.pn(a)));
+    const double g1 = RN_ADD(lo.gt(a, e1), hi.gt(a, e1)), g2 = RN_ADD(lo.gt(a, e2), hi.gt(a, e2));
+    const double ga2 = RN_FMA(g2, g2, RN_FMA(g1, g1, RN_MUL(gn, gn)));
+    if (PF_ZERO(pal) || PF_ZERO(ga2) || PF_ZERO(pd)) return;
+    const double dot = RN_FMA(g2, l2, RN_FMA(g1, l1, RN_MUL(gn, ln)));
     const double x = RN_MUL(RN_MUL(pal, gl2), RN_MUL(ga2, ga2));
     double r;
-    if (x >= 0x1.0p-1000 && x <= 0x1.0p+1000) {
-      r = rsqrt(x);
+    if (!exp_outside(x, 1000)) {
+      r = rsqrt_nr(x);
     } else {  // extreme magnitudes: factorised (never taken for O(1) fields)
       const double ra = rsqrt(ga2);
       r = RN_MUL(RN_MUL(rsqrt(pal), rsqrt(gl2)), RN_MUL(ra, ra));
     }
-    const double w = RN_MUL(RN_MUL(RN_MUL(RN_MUL(kp.pi_eps_4, pb[a]), RN_MUL(hl, pd)), RN_MUL(dot, gfa[d])), r);
-    J0 = RN_FMA(w, RN_MUL(0.5, RN_ADD(lo.dcl(a, 0), hi.dcl(a, 0))), J0);
-    J1 = RN_FMA(w, RN_MUL(0.5, RN_ADD(lo.dcl(a, 1), hi.dcl(a, 1))), J1);
+    const double w = RN_MUL(RN_MUL(RN_MUL(RN_MUL(khl, saa), pd), RN_MUL(dot, gn)), r);
+    double dc0, dc1;
+    if (d < 2) {
+      const double *t = lo.tab();
+#if PF_MU_HOIST
+      dc0 = RN_FMA(ms0, t[T_DI2A + a * 2], t[T_DCHAT2 + a * 2]);
+      dc1 = RN_FMA(ms1, t[T_DI2A + a * 2 + 1], t[T_DCHAT2 + a * 2 + 1]);
+#else
+      dc0 = RN_FMA(RN_ADD(lo.mu(0), hi.mu(0)), t[T_DI2A + a * 2], t[T_DCHAT2 + a * 2]);
+      dc1 = RN_FMA(RN_ADD(lo.mu(1), hi.mu(1)), t[T_DI2A + a * 2 + 1], t[T_DCHAT2 + a * 2 + 1]);
+#endif
+    } else {
+      dc0 = RN_ADD(lo.dcl(a, 0), hi.dcl(a, 0));
+      dc1 = RN_ADD(lo.dcl(a, 1), hi.dcl(a, 1));
+    }
+    J0 = RN_FMA(w, dc0, J0);
+    J1 = RN_FMA(w, dc1, J1);
+  };
+  if (ROLL) {
+#pragma unroll 1
+    for (int a = 0; a < 3; ++a) solid(a);
+  } else {
+    solid(0);
+    solid(1);
+    solid(2);
   }
   out[0] = RN_SUB(out[0], J0);
   out[1] = RN_SUB(out[1], J1);
@@ -541,6 +632,7 @@ struct MuQAcc {  // accessor over a register MuQ
   __device__ __forceinline__ double M(int c) const { return q.M[c]; }
   __device__ __forceinline__ double mu(int c) const { return q.mu[c]; }
   __device__ __forceinline__ double dcl(int a, int c) const { return q.dcl[a][c]; }
+  __device__ __forceinline__ const double *tab() const { return q.tab; }
 };
 
 __device__ __forceinline__ void mu_face(const KParams &kp, const MuQ &lo, const MuQ &hi, int d, double out[NMU]) {

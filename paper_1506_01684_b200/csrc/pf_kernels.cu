@@ -41,6 +41,7 @@ __global__ void table_kernel(double *tab, int64_t nplanes, TabParams tp, int64_t
     for (int c = 0; c < NMU; ++c) {
       row[T_DI2A + a * 2 + c] = row[T_INV2A + LIQ * 2 + c] - row[T_INV2A + a * 2 + c];
       row[T_DCHAT + a * 2 + c] = row[T_CHAT + LIQ * 2 + c] - row[T_CHAT + a * 2 + c];
+      row[T_DCHAT2 + a * 2 + c] = 2.0 * row[T_DCHAT + a * 2 + c];   // exact
     }
 }
 
@@ -123,7 +124,11 @@ __device__ __forceinline__ void load_muq(const KParams &kp, const BlockView &b, 
   mu[0] = __ldg(b.mu[0] + o);
   mu[1] = __ldg(b.mu[1] + o);
   mu_cell_q(tabrow, po, pn, mu, q);
-  centre_grads(kp, b.phin, o, st, q.gn, skip);
+#pragma unroll
+  for (int e = 0; e < 3; ++e)   // raw centre differences (mu_face_t is scale-free in them)
+#pragma unroll
+    for (int a = 0; a < NPH; ++a)
+      q.gn[a][e] = (e == skip) ? 0.0 : cdiff(__ldg(b.phin[a] + o - st[e]), __ldg(b.phin[a] + o + st[e]));
 }
 
 __global__ void __launch_bounds__(128) mu_naive_kernel(KParams kp, BlockView b) {

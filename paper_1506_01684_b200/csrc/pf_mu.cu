@@ -40,9 +40,17 @@ struct __align__(128) MuSmem {
   uint32_t wflat[3][NTHR / 32];   // per-warp flatness votes of a staged phi^{n+1}_l plane
 };
 #ifndef PF_MU_UNROLL
-#define PF_MU_UNROLL 4
+#define PF_MU_UNROLL 2
 #endif
-constexpr int kMuUnroll = PF_MU_UNROLL;   // plane-loop unroll: 4 makes every slot index static (measured: 2 -> 4 -0.8 %)
+#ifndef PF_MU_ROLL
+#define PF_MU_ROLL 1
+#endif
+// x/y faces (both cells in shared memory): the three solids of the
+// anti-trapping current in a loop that is not unrolled — a third of the
+// code (measured on the all-guards-open state: 13.6 -> 10.8 ms; C4 unchanged)
+constexpr bool kMuRoll = PF_MU_ROLL != 0;
+constexpr int kMuUnroll = PF_MU_UNROLL;   // plane-loop unroll (round 1: 2 -> 4 -0.8 %; with the rolled anti-trapping
+                                          // solids 4 costs registers: C4 3.78 vs 3.15 ms, interface 11.8 vs 11.2 ms)
 constexpr int NBOX = RX * RY;     // staged cells of a plane tile (interior + ring + corners)
 static_assert(NBOX <= 2 * NTHR, "flatness check covers the box in two passes");
 #define T(arr, row, col) TILE_AT(arr, row, col)
@@ -55,18 +63,19 @@ struct RawQ {
   const MuSmem &S;
   const KParams &kp;
   int snm, sn, snp, s2, col, row;
-  const double *tab;
+  const double *tb;
   double Mv[NMU];
   __device__ __forceinline__ double pn(int a) const { return T(S.pn[sn][a], row, col); }
   __device__ __forceinline__ double dp(int a) const { return RN_SUB(T(S.pn[sn][a], row, col), T(S.po[s2][a], row, col)); }
   __device__ __forceinline__ double gt(int a, int e) const {
-    if (e == 0) return cgrad(kp, T(S.pn[sn][a], row, col - 1), T(S.pn[sn][a], row, col + 1));
-    if (e == 1) return cgrad(kp, T(S.pn[sn][a], row - 1, col), T(S.pn[sn][a], row + 1, col));
-    return cgrad(kp, T(S.pn[snm][a], row, col), T(S.pn[snp][a], row, col));
+    if (e == 0) return cdiff(T(S.pn[sn][a], row, col - 1), T(S.pn[sn][a], row, col + 1));
+    if (e == 1) return cdiff(T(S.pn[sn][a], row - 1, col), T(S.pn[sn][a], row + 1, col));
+    return cdiff(T(S.pn[snm][a], row, col), T(S.pn[snp][a], row, col));
   }
   __device__ __forceinline__ double M(int c) const { return Mv[c]; }
   __device__ __forceinline__ double mu(int c) const { return T(S.mu[s2][c], row, col); }
-  __device__ __forceinline__ double dcl(int a, int c) const { return dcl_of(tab, a, c, mu(c)); }
+  __device__ __forceinline__ double dcl(int a, int c) const { return dcl_of(tb, a, c, mu(c)); }
+  __device__ __forceinline__ const double *tab() const { return tb; }
 };
 
 // Accessor for the own column's cell at plane k+1 (the upper cell of the
@@ -77,18 +86,19 @@ struct ColQ {
   const MuSmem &S;
   const KParams &kp;
   int sc, col, row;
-  const double *tab;
+  const double *tb;
   const double *po, *muv;
   double Mv[NMU];
   __device__ __forceinline__ double pn(int a) const { return T(S.pn[sc][a], row, col); }
   __device__ __forceinline__ double dp(int a) const { return RN_SUB(T(S.pn[sc][a], row, col), po[a]); }
   __device__ __forceinline__ double gt(int a, int e) const {
-    if (e == 0) return cgrad(kp, T(S.pn[sc][a], row, col - 1), T(S.pn[sc][a], row, col + 1));
-    return cgrad(kp, T(S.pn[sc][a], row - 1, col), T(S.pn[sc][a], row + 1, col));  // e == 1 (z-face: e != 2)
+    if (e == 0) return cdiff(T(S.pn[sc][a], row, col - 1), T(S.pn[sc][a], row, col + 1));
+    return cdiff(T(S.pn[sc][a], row - 1, col), T(S.pn[sc][a], row + 1, col));  // e == 1 (z-face: e != 2)
   }
   __device__ __forceinline__ double M(int c) const { return Mv[c]; }
   __device__ __forceinline__ double mu(int c) const { return muv[c]; }
-  __device__ __forceinline__ double dcl(int a, int c) const { return dcl_of(tab, a, c, muv[c]); }
+  __device__ __forceinline__ double dcl(int a, int c) const { return dcl_of(tb, a, c, muv[c]); }
+  __device__ __forceinline__ const double *tab() const { return tb; }
 };
 
 // MODE: MU_FULL the whole mu update (Algorithm 1); MU_LOCAL everything but the
@@ -178,8 +188,8 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
     mu_cell_q(S.tab[sc], po, pn, mu, q);
 #pragma unroll
     for (int a = 0; a < NPH; ++a) {
-      q.gn[a][0] = cgrad(kp, T(S.pn[sc][a], orow, oc - 1), T(S.pn[sc][a], orow, oc + 1));
-      q.gn[a][1] = cgrad(kp, T(S.pn[sc][a], orow - 1, oc), T(S.pn[sc][a], orow + 1, oc));
+      q.gn[a][0] = cdiff(T(S.pn[sc][a], orow, oc - 1), T(S.pn[sc][a], orow, oc + 1));
+      q.gn[a][1] = cdiff(T(S.pn[sc][a], orow - 1, oc), T(S.pn[sc][a], orow + 1, oc));
       q.gn[a][2] = 0.0;
     }
   };
@@ -310,7 +320,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
         RawQ lo = rawq(k, oc - 1, orow), hi = rawq(k, oc, orow);
         lo.Mv[0] = S.M[0][orow][oc - 1]; lo.Mv[1] = S.M[1][orow][oc - 1];
         hi.Mv[0] = Mown[0]; hi.Mv[1] = Mown[1];
-        mu_face_t<MODE == MU_FULL>(kp, lo, hi, 0, fxo);
+        mu_face_t<MODE == MU_FULL, kMuRoll>(kp, lo, hi, 0, fxo);
         S.fx[0][ty][tx] = fxo[0];
         S.fx[1][ty][tx] = fxo[1];
       }
@@ -318,7 +328,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
         RawQ lo = rawq(k, oc, orow - 1), hi = rawq(k, oc, orow);
         lo.Mv[0] = S.M[0][orow - 1][oc]; lo.Mv[1] = S.M[1][orow - 1][oc];
         hi.Mv[0] = Mown[0]; hi.Mv[1] = Mown[1];
-        mu_face_t<MODE == MU_FULL>(kp, lo, hi, 1, fyo);
+        mu_face_t<MODE == MU_FULL, kMuRoll>(kp, lo, hi, 1, fyo);
         S.fy[0][ty][tx] = fyo[0];
         S.fy[1][ty][tx] = fyo[1];
       }
@@ -329,7 +339,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
         RawQ lo = rawq(k, c0, r0), hi = rawq(k, c1, r1);
         lo.Mv[0] = S.M[0][r0][c0]; lo.Mv[1] = S.M[1][r0][c0];
         hi.Mv[0] = S.M[0][r1][c1]; hi.Mv[1] = S.M[1][r1][c1];
-        mu_face_t<MODE == MU_FULL>(kp, lo, hi, d, f);
+        mu_face_t<MODE == MU_FULL, kMuRoll>(kp, lo, hi, d, f);
         if (d == 0) { S.fx[0][r0 - 1][TX] = f[0]; S.fx[1][r0 - 1][TX] = f[1]; }
         else { S.fy[0][TY][c0 - 1] = f[0]; S.fy[1][TY][c0 - 1] = f[1]; }
       }

@@ -1050,7 +1050,6 @@ pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
   // kernel constants
   KParams &kp = c->kp;
   kp.dt = p->dt; kp.inv_dt = 1.0 / p->dt; kp.inv_dx = 1.0 / p->dx; kp.inv_2dx = 1.0 / (2.0 * p->dx);
-  kp.half_inv_dt = 0.5 / p->dt;
   for (int a = 0; a < 4; ++a) {
     kp.dt_taueps[a] = p->dt / (p->tau[a] * p->eps);
     kp.g3[a] = p->gamma3[a];
@@ -1062,7 +1061,7 @@ pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
     kp.omp[q] = 16.0 / (M_PI * M_PI) * p->gamma[pair_a(q)][pair_b(q)];
     kp.delta[q] = p->aniso ? p->delta[pair_a(q)][pair_b(q)] : 0.0;
   }
-  kp.pi_eps_4 = M_PI * p->eps / 4.0;
+  kp.pi_eps_16dt = M_PI * p->eps / (16.0 * p->dt);
   kp.Gv = p->G * p->v;
   kp.aniso = p->aniso ? 1 : 0;
   kp.shortcuts = p->shortcuts ? 1 : 0;

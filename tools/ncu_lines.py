@@ -5,6 +5,7 @@ Maps SASS offsets to source lines with `nvdisasm -g` (needs -lineinfo)."""
 import csv, io, re, subprocess, sys
 rep, kre, cubin, fn = sys.argv[1:5]
 top = int(sys.argv[5]) if len(sys.argv) > 5 else 40
+by_inst = len(sys.argv) > 6 and sys.argv[6] == "inst"   # rank lines by executed instructions
 sass = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout
 sec = sass.split(f".text.{fn}:")[1].split("//---------------------")[0]
 line_of = {}
@@ -43,7 +44,8 @@ for (f, l) in agg:
                 srcs[f] = open(root + f).read().splitlines()
             except OSError:
                 srcs[f] = []
-for key, w in sorted(agg.items(), key=lambda kv: -kv[1])[:top]:
+order = sorted(agg.items(), key=(lambda kv: -inst[kv[0]]) if by_inst else (lambda kv: -kv[1]))
+for key, w in order[:top]:
     f, l = key
     txt = srcs.get(f, [])[l - 1].strip() if 0 < l <= len(srcs.get(f, [])) else ""
     print(f"{100 * w / tot:5.1f}%  inst {inst[key]:12.0f}  {f}:{l:<4d} {txt[:90]}")
