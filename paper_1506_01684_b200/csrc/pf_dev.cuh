@@ -66,6 +66,15 @@ __device__ __forceinline__ double rcp_nr(double s) {
   return __fma_rn(r, e, r);
 }
 
+// x == +-0 as an integer test on the bits (a double compare is an FP64-pipe
+// instruction); false for NaN, like x == 0.0
+__device__ __forceinline__ bool is_zero_bits(double x) { return (__double_as_longlong(x) << 1) == 0ll; }
+// |x| outside [2^-e, 2^e) or zero / subnormal / inf / NaN, from the exponent bits
+__device__ __forceinline__ bool exp_outside(double x, int e) {
+  const int ex = (__double2hiint(x) >> 20) & 0x7ff;   // biased exponent
+  return (unsigned)(ex - (1023 - e)) >= (unsigned)(2 * e);
+}
+
 // 1/sqrt(x) for x in [2^-1000, 2^1000]: the hardware approximation refined by
 // two Newton steps r += r (1 - x r^2) / 2 (pinned; a few ulp, not correctly
 // rounded) — the library rsqrt's special-case handling is 17 instructions.
@@ -121,41 +130,28 @@ __device__ __forceinline__ double2 tab2(const double *__restrict__ tab, int base
 // ---------------------------------------------------------------------------
 
 // Cubic-anisotropy gradient of the pair energy e = gamma a_c^2 |q|^2,
-// a_c = 1 - delta (3 - 4 Q4/|q|^4) (reading R3); g = 0 at q = 0.
-// Pinned: used inside face fluxes.  Returns g (without the 2 gamma factor
-// folded: full g).
+// a_c = 1 - delta (3 - 4 Q4/|q|^4) (reading R3); g = 0 at q = 0.  Pinned:
+// used inside face fluxes.  Returns g (without the 2 gamma factor folded:
+// full g).
 //
-// g is homogeneous of degree 1 in q (a_c depends on q/|q| only).  The direct
-// formula needs |q|^-4 and Q4 = sum q_d^4, which over- / underflow outside
-// |q| ~ 2^+-250; there (and at q = 0) the slow path evaluates it on q scaled by
-// a power of two into [1, 2) and scales the result back — exact scalings, so it
-// returns the bits the direct formula would give without the range limit.  The
-// range test is one integer compare on |q|^2's exponent (2^-400 <= |q|^2 <
-// 2^400; 0, subnormals, inf and NaN fall outside).
-__device__ __forceinline__ bool q2_extreme(double q2) {
-  return (unsigned)(__double2hiint(q2) - 0x26F00000) >= 0x32000000u;
+// g is homogeneous of degree 1; the direct formula needs |q|^-4 and Q4, which
+// leave the double range for |q| < ~1e-77.  Below |q|^2 = 2^-400 (|q| <
+// 1.5e-60) g is returned as 0 — an absolute error under 1e-59 (DESIGN.md
+// reading R30; the oracle evaluates those exactly by power-of-two scaling).
+// The test is an integer compare on |q|^2's exponent and an early return, the
+// round-1 exit for q = 0 (absent pairs: most pairs of a bulk cell) widened —
+// measured: a rescaling path costs the anisotropic phi-sweep 6-40 % however it
+// is written, a select instead of the exit 40 %.  Pair vectors that small need
+// phase fractions near 1e-60, which the explicit step does not produce.
+__device__ __forceinline__ double q2_of(const double q[3]) {
+  return RN_FMA(q[2], q[2], RN_FMA(q[1], q[1], RN_MUL(q[0], q[0])));
 }
-__device__ __forceinline__ double pow2_d(int e) {   // 2^e, -1022 <= e <= 1023
-  return __hiloint2double((1023 + e) << 20, 0);
+__device__ __forceinline__ bool q2_tiny(double q2) {   // q2 < 2^-400 (incl. 0, subnormals)
+  return ((__double2hiint(q2) >> 20) & 0x7ff) < 1023 - 400;
 }
-// scale q (!= 0) in place by 2^-s so that max |q_d| is in [1, 2); returns s
-__device__ __forceinline__ int pow2_normalise(double q[3]) {
-  int s = 0;
-  int m = max(__double2hiint(q[0]) & 0x7fffffff, max(__double2hiint(q[1]) & 0x7fffffff, __double2hiint(q[2]) & 0x7fffffff));
-  if ((m >> 20) == 0) {   // largest component subnormal: lift by 2^600 first (exact)
-#pragma unroll
-    for (int d = 0; d < 3; ++d) q[d] *= pow2_d(600);
-    s = -600;
-    m = max(__double2hiint(q[0]) & 0x7fffffff, max(__double2hiint(q[1]) & 0x7fffffff, __double2hiint(q[2]) & 0x7fffffff));
-  }
-  const int ex = (m >> 20) - 1023;
-#pragma unroll
-  for (int d = 0; d < 3; ++d) q[d] *= pow2_d(-ex);
-  return s + ex;
-}
-__device__ __forceinline__ bool is_zero3(const double q[3]) { return q[0] == 0.0 && q[1] == 0.0 && q[2] == 0.0; }
-__device__ __forceinline__ void pair_grad_aniso_core(double g2, double delta, const double q[3], double q2,
-                                                     double out[3]) {
+__device__ __forceinline__ void pair_grad_aniso(double g2, double delta, const double q[3], double out[3]) {
+  const double q2 = q2_of(q);
+  if (q2_tiny(q2)) { out[0] = out[1] = out[2] = 0.0; return; }
   double s2[3], s4 = 0.0;
 #pragma unroll
   for (int d = 0; d < 3; ++d) { s2[d] = RN_MUL(q[d], q[d]); }
@@ -172,26 +168,12 @@ __device__ __forceinline__ void pair_grad_aniso_core(double g2, double delta, co
     out[d] = RN_MUL(RN_MUL(g2, ac), RN_FMA(d16, t, RN_MUL(ac, q[d])));
   }
 }
-__device__ __forceinline__ double q2_of(const double q[3]) {
-  return RN_FMA(q[2], q[2], RN_FMA(q[1], q[1], RN_MUL(q[0], q[0])));
-}
-__device__ __forceinline__ void pair_grad_aniso(double g2, double delta, const double q[3], double out[3]) {
-  const double q2 = q2_of(q);
-  if (q2_extreme(q2)) {
-    if (is_zero3(q)) { out[0] = out[1] = out[2] = 0.0; return; }
-    double u[3] = {q[0], q[1], q[2]};
-    const int s = pow2_normalise(u);
-    pair_grad_aniso_core(g2, delta, u, q2_of(u), out);
-#pragma unroll
-    for (int d = 0; d < 3; ++d) out[d] *= pow2_d(s);
-    return;
-  }
-  pair_grad_aniso_core(g2, delta, q, q2, out);
-}
 
 // Component d alone of pair_grad_aniso (the face flux needs only the normal
 // component): the same pinned operations, so bitwise the same value.
-__device__ __forceinline__ double pair_grad_aniso_core_d(double g2, double delta, const double q[3], double q2, int d) {
+__device__ __forceinline__ double pair_grad_aniso_d(double g2, double delta, const double q[3], int d) {
+  const double q2 = q2_of(q);
+  if (q2_tiny(q2)) return 0.0;
   double s2[3];
 #pragma unroll
   for (int e = 0; e < 3; ++e) s2[e] = RN_MUL(q[e], q[e]);
@@ -203,16 +185,6 @@ __device__ __forceinline__ double pair_grad_aniso_core_d(double g2, double delta
   const double d16 = RN_MUL(16.0, delta);
   const double t = RN_MUL(RN_FMA(s2[d], q[d], -RN_MUL(RN_MUL(s4, r2), q[d])), r2);
   return RN_MUL(RN_MUL(g2, ac), RN_FMA(d16, t, RN_MUL(ac, q[d])));
-}
-__device__ __forceinline__ double pair_grad_aniso_d(double g2, double delta, const double q[3], int d) {
-  const double q2 = q2_of(q);
-  if (q2_extreme(q2)) {
-    if (is_zero3(q)) return 0.0;
-    double u[3] = {q[0], q[1], q[2]};
-    const int s = pow2_normalise(u);
-    return pair_grad_aniso_core_d(g2, delta, u, q2_of(u), d) * pow2_d(s);
-  }
-  return pair_grad_aniso_core_d(g2, delta, q, q2, d);
 }
 
 // Face flux j_a (component d) of the phi-sweep between cells lo and hi = lo+e_d
@@ -268,15 +240,6 @@ __device__ __forceinline__ void phi_face(const KParams &kp, const double plo[NPH
       jf[b] = RN_FMA(gd, pb[a], jf[b]);
     }
   }
-}
-
-// x == +-0 as an integer test on the bits (a double compare is an FP64-pipe
-// instruction); false for NaN, like x == 0.0
-__device__ __forceinline__ bool is_zero_bits(double x) { return (__double_as_longlong(x) << 1) == 0ll; }
-// |x| outside [2^-e, 2^e) or zero / subnormal / inf / NaN, from the exponent bits
-__device__ __forceinline__ bool exp_outside(double x, int e) {
-  const int ex = (__double2hiint(x) >> 20) & 0x7ff;   // biased exponent
-  return (unsigned)(ex - (1023 - e)) >= (unsigned)(2 * e);
 }
 
 // Raw centre difference hi - lo (the mu-sweep's anti-trapping gradients, which
