@@ -93,6 +93,17 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 // driving force vanishes (S = 1, psi-bar = psi_p), and the projection maps
 // 1 + dt/(tau eps) mean back to exactly 1 (Sterbenz) and the pushed-down
 // absent phases to exactly 0 — so skipping it is exact.
+// the same test on the bits (integer pipe): one component 1.0, the others +-0
+__device__ __forceinline__ bool is_vertex_bits(const double p[NPH]) {
+  int ones = 0, zeros = 0;
+#pragma unroll
+  for (int a = 0; a < NPH; ++a) {
+    const unsigned long long v = __double_as_longlong(p[a]);
+    ones += v == 0x3FF0000000000000ull;
+    zeros += (v << 1) == 0ull;
+  }
+  return ones == 1 && zeros == NPH - 1;
+}
 __device__ __forceinline__ bool is_vertex(const double p[NPH]) {
   int ones = 0, zeros = 0;
 #pragma unroll

@@ -32,7 +32,7 @@ struct __align__(128) PhiSmem {
 
 constexpr uint32_t PHI_STAGE_BYTES = (NPH * RXS * RY + TAB) * 8;
 
-template <bool ANISO, bool SC>
+template <bool ANISO, int SC>   // SC: 0 no shortcut code, 1 the round-1 vote (run-time flag), 2 skip-faces shortcuts
 #ifndef PF_PHI_MINB
 #define PF_PHI_MINB (512 / NTHR)
 #endif
@@ -142,6 +142,39 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
     //   dpart = ((jz+ - jz-) - jx-) - jy-,   rhs = (r0 - c dpart) - c (jx+ + jy+)
     // with c = eps T / dx (the oracle's O4.6 sum in another order: equal up to
     // rounding; the anisotropic kernel forms dpart after the barrier).
+    // region shortcut, SC = 2 (NEXT-1): voted
+    // before the faces with integer compares on the bits (a double compare is
+    // an FP64-pipe instruction), in two stages (own cell a simplex vertex, then
+    // its D3C7 / D3C19 neighbours identical).  A shortcut warp's own faces are
+    // exactly 0 (2x2 determinants and differences of equal 0/1 values), so it
+    // writes zeros instead of evaluating them and keeps phi^{n+1} = phi^n,
+    // bitwise what the full update returns (is_vertex).  Slots k-1..k+1 are
+    // resident; slot(k-1) is refilled only after barrier B(k).
+    bool skip2 = false;
+    if (SC == 2) {
+      double pcv[NPH];
+#pragma unroll
+      for (int a = 0; a < NPH; ++a) pcv[a] = T(S.p[sc][a], orow, oc);
+      if (__all_sync(0xffffffffu, is_vertex_bits(pcv) || !active)) {
+        auto same = [](double x, double v) { return __double_as_longlong(x) == __double_as_longlong(v); };
+        bool mine = true;
+#pragma unroll
+        for (int a = 0; a < NPH; ++a) {
+          const double v = pcv[a];
+          mine = mine && same(T(S.p[sc][a], orow, oc - 1), v) && same(T(S.p[sc][a], orow, oc + 1), v) &&
+                 same(T(S.p[sc][a], orow - 1, oc), v) && same(T(S.p[sc][a], orow + 1, oc), v) &&
+                 same(T(S.p[sm][a], orow, oc), v) && same(T(S.p[sp][a], orow, oc), v);
+          if (ANISO)
+            mine = mine && same(T(S.p[sc][a], orow - 1, oc - 1), v) && same(T(S.p[sc][a], orow - 1, oc + 1), v) &&
+                   same(T(S.p[sc][a], orow + 1, oc - 1), v) && same(T(S.p[sc][a], orow + 1, oc + 1), v) &&
+                   same(T(S.p[sm][a], orow, oc - 1), v) && same(T(S.p[sm][a], orow, oc + 1), v) &&
+                   same(T(S.p[sm][a], orow - 1, oc), v) && same(T(S.p[sm][a], orow + 1, oc), v) &&
+                   same(T(S.p[sp][a], orow, oc - 1), v) && same(T(S.p[sp][a], orow, oc + 1), v) &&
+                   same(T(S.p[sp][a], orow - 1, oc), v) && same(T(S.p[sp][a], orow + 1, oc), v);
+        }
+        skip2 = __all_sync(0xffffffffu, mine || !active) != 0;
+      }
+    }
     double pc[NPH], pp[NPH], jzp[NPH], dpart[NPH];
     if (!ANISO)
 #pragma unroll
@@ -174,6 +207,18 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
           }
         }
       };
+      if (SC == 2 && skip2) {   // a shortcut warp: its own faces are exactly 0; the far faces as usual
+#pragma unroll
+        for (int a = 0; a < NPH; ++a) {
+          pc[a] = T(S.p[sc][a], orow, oc);
+          jzp[a] = 0.0;
+          dpart[a] = 0.0;
+          if (!ANISO) jzm[a] = 0.0;
+          S.fx[fb][a][ty][tx] = 0.0;
+          S.fy[fb][a][ty][tx] = 0.0;
+        }
+        far_faces();
+      } else {
       if (!ANISO) far_faces();
       if (ANISO) {   // anisotropic: the z-face k+1/2 first too (its dpart is formed after the barrier; -0.4 %)
 #pragma unroll
@@ -212,12 +257,13 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
         }
       }
       if (ANISO) far_faces();
+      }
     }
     // region shortcut (NEXT-1): a warp whose cells
     // are all simplex vertices with an identical D3C7 (D3C19) neighbourhood
     // keeps phi^{n+1} = phi^n — bitwise what the full update returns (is_vertex)
     auto bulk_warp = [&]() {
-      if (!SC || !kp.shortcuts) return false;   // SC = false: the check compiled out
+      if (SC != 1 || !kp.shortcuts) return false;   // SC = 0: the check compiled out
       bool mine = is_vertex(pc);
 #pragma unroll
       for (int a = 0; a < NPH; ++a) {
@@ -237,7 +283,7 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
     };
     // the vote reads slot(k-1), which stage(k+3) refills right after B(k): it
     // is taken before the barrier in both kernels
-    const bool skip = bulk_warp();
+    const bool skip = SC == 2 ? skip2 : bulk_warp();
     // isotropic: the cell terms that need no face flux (phi_cell_rhs0, on the
     // raw centre differences) are formed before the barrier, where the tile
     // values are still at hand; the anisotropic kernel has no registers to
@@ -294,11 +340,12 @@ static int g_phi_slots[2] = {1, 1};   // resident CTAs on the GPU, [ANISO]
 
 void prepare_phi_tiled() {
   const int sm = (int)sizeof(PhiSmem);
-  cudaFuncSetAttribute(phi_tiled_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(phi_tiled_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(phi_tiled_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  g_phi_slots[0] = grid_slots(phi_tiled_kernel<false, true>, NTHR, sm);
-  g_phi_slots[1] = grid_slots(phi_tiled_kernel<true, false>, NTHR, sm);
+  cudaFuncSetAttribute(phi_tiled_kernel<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(phi_tiled_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(phi_tiled_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(phi_tiled_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  g_phi_slots[0] = grid_slots(phi_tiled_kernel<false, 1>, NTHR, sm);
+  g_phi_slots[1] = grid_slots(phi_tiled_kernel<true, 0>, NTHR, sm);
 }
 
 void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm) {
@@ -309,12 +356,19 @@ void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, con
   const int kz = chunk_z(b.nz, gx * gy, g_phi_slots[kp.aniso ? 1 : 0], PF_PHI_WAVES, false);
   dim3 grd(gx, gy, (b.nz + kz - 1) / kz), blk(TX, TY);
   const size_t sm = sizeof(PhiSmem);
-  // the anisotropic kernel without the shortcut check when it is off (-3 %); the
-  // isotropic one keeps the run-time check (its code without it measured +4 %:
-  // the compiler's schedule, not the check, decides there)
-  if (kp.aniso && kp.shortcuts) phi_tiled_kernel<true, true><<<grd, blk, sm, s>>>(tm, kp, b, kz);
-  else if (kp.aniso) phi_tiled_kernel<true, false><<<grd, blk, sm, s>>>(tm, kp, b, kz);
-  else phi_tiled_kernel<false, true><<<grd, blk, sm, s>>>(tm, kp, b, kz);
+  // shortcuts on: the skip-faces kernels (SC = 2).  Off: the anisotropic kernel
+  // without any shortcut code (-3 %), the isotropic one with the round-1
+  // run-time check compiled in (its code without it, or with the SC = 2 vote
+  // in the same kernel, measured +1.7 %: the compiler's schedule, not the
+  // check, decides there)
+  if (kp.shortcuts) {
+    if (kp.aniso) phi_tiled_kernel<true, 2><<<grd, blk, sm, s>>>(tm, kp, b, kz);
+    else phi_tiled_kernel<false, 2><<<grd, blk, sm, s>>>(tm, kp, b, kz);
+  } else if (kp.aniso) {
+    phi_tiled_kernel<true, 0><<<grd, blk, sm, s>>>(tm, kp, b, kz);
+  } else {
+    phi_tiled_kernel<false, 1><<<grd, blk, sm, s>>>(tm, kp, b, kz);
+  }
 }
 
 }  // namespace pf
