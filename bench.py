@@ -296,6 +296,30 @@ def run_gpu(args):
     launches = int(ctx.info().launches - l0) // max(1, args.reps)
     order = sorted(range(len(windows)), key=lambda i: windows[i][0])
     ms, ms_phi, ms_mu = windows[order[len(order) // 2]]
+    # the same windows' length with the region shortcuts on (NEXT-1; bitwise the
+    # same results, pf_set_shortcuts): reported beside the headline, which keeps
+    # them off so that its FLOP count per cell is exact
+    sc = None
+    if not args.graph and not args.no_shortcuts:
+        ctx.set_shortcuts(True)
+        ctx.set_timing(True)
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        ctx.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        inf = ctx.info()
+        sc_ms = max_over_ranks(e0.elapsed_time(e1))
+        sc = {"value": round(cells_local * world * args.steps / (sc_ms / 1e3) / 1e6, 2),
+              "ms_per_step": round(sc_ms / args.steps, 4),
+              "phi_ms": round(inf.ms_phi / max(1, inf.phi_launches), 4),
+              "mu_ms": round(inf.ms_mu / max(1, inf.mu_launches), 4),
+              "what": "region shortcuts on (pf_set_shortcuts): bitwise-identical results; the headline keeps them "
+                      "off for the exact FLOP count"}
+        ctx.set_shortcuts(False)
+        ctx.set_timing(False)
     if args.graph:
         ctx.set_timing(True)
         ctx.step(min(args.steps, 10))
@@ -440,6 +464,7 @@ def run_gpu(args):
                             "overlapped in z-slabs (single block per GPU; else pf_write + pf_step(1) + pf_read)",
                     "job": {"value": round(e2e_job, 2) if e2e_job else None, "steps": args.steps,
                             "what": "pf_write(pinned host state) once + pf_step(steps) + pf_read(pinned host) once"}},
+            "shortcuts": sc,
             "gpu_launches": launches,
             "clocks": clk,
         }
@@ -495,6 +520,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--reps", type=int, default=3, help="timed windows of --steps steps each; the median is reported")
     ap.add_argument("--no-interface", action="store_true", help="skip the all-guards-open sweep measurement")
+    ap.add_argument("--no-shortcuts", action="store_true", help="skip the region-shortcut window")
     ap.add_argument("--graph", action="store_true", help="replay each step as a CUDA graph (single rank)")
     ap.add_argument("--grid", type=int, nargs=3, metavar=("NX", "NY", "NZ"),
                     help="global grid overriding the config's (its physics and init recipe kept)")

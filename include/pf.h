@@ -113,8 +113,13 @@ typedef struct {
                                    anti-trapping current), then mu-sweep-neighbor
                                    adds its divergence (Algorithm 2's split); the
                                    mu halo is not hidden;
-                                 3: both (Algorithm 2).
-                                 Results of 2/3 differ from 0/1 by rounding only. */
+                                 3: both (Algorithm 2);
+                                 4: both without Algorithm 2's second pass: the
+                                   mu-sweep over the tiles that read no ghost
+                                   beside the phi halo, the shell (boundary tiles,
+                                   cap planes) after it; the mu halo as in 0.
+                                 Results of 2/3 differ from 0/1 by rounding only;
+                                 4 equals 0/1 bit for bit. */
   int32_t graph;              /* 1: single-rank runs without per-sweep timing replay
                                  each step as a CUDA graph (one launch per step);
                                  0 (default): launch the kernels one by one, which
@@ -264,6 +269,14 @@ pf_status pf_mesh_table(int8_t *out);
 
 /* Enable (1) / disable (0) per-sweep CUDA-event timing; resets the timers. */
 pf_status pf_set_timing(pf_ctx *c, int32_t on);
+
+/* Switch the region shortcuts (pf_params.shortcuts, NEXT-1: PAPER.md:281-290,
+ * 483-492) on (1) or off (0) for the following steps.  Results are bitwise the
+ * same either way (tests/test_gpu_parity.py, test_gpu_trajectories.py); on is
+ * faster on every measured block type (profiles/r02_scenarios.md), off is the
+ * configuration whose FLOP count per cell is exact.
+ * Errors: PF_ERR_ARG (NULL), PF_ERR_STATE after an error. */
+pf_status pf_set_shortcuts(pf_ctx *c, int32_t on);
 
 pf_status pf_info(pf_ctx *c, pf_info_t *out);
 

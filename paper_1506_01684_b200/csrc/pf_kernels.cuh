@@ -49,6 +49,8 @@ struct BlockView {
   int64_t pitch, plane;
   const double *tab;        // table row of local plane k = 0
   int zoff;                 // allocation plane of local k = 0 (1 + window offset), for TMA
+  int tile_x0, tile_y0;     // first CTA tile of a launch over a tile sub-range (mu-sweep
+                            // interior / shell split, overlap mode 4); 0 otherwise
 };
 
 // Strided 3D box copy (halo exchange: local copy, pack, unpack).
@@ -97,6 +99,12 @@ void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, con
 // part that adds its divergence after the phi^{n+1} halo exchange
 enum { MU_FULL = 0, MU_LOCAL = 1, MU_NEIGHBOR = 2 };
 void launch_mu_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm, int mode = MU_FULL);
+// the mu-sweep over CTA tiles [tx0, tx1) x [ty0, ty1) of the block (b may be a
+// z-slab view): bitwise the cells' values of the whole-block launch
+void launch_mu_tiles(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm, int tx0, int tx1,
+                     int ty0, int ty1);
+int mu_tiles_x(int nx);   // CTA tiles of the mu-sweep along x / y
+int mu_tiles_y(int ny);
 void launch_copy(cudaStream_t s, const CopyOp *d_ops, int nops, int64_t nctas);
 void launch_init(cudaStream_t s, const InitSpec &is, double *const phi[NPH], double *const mu[NMU],
                  int nx, int ny, int nz, int64_t pitch, int64_t plane, int64_t x0, int64_t y0, int64_t z0);

@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
   extern __shared__ __align__(128) unsigned char smem_raw[];
   MuSmem &S = *reinterpret_cast<MuSmem *>(smem_raw);
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
-  const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
+  const int i0 = (blockIdx.x + b.tile_x0) * TX, j0 = (blockIdx.y + b.tile_y0) * TY;
   const int k0 = blockIdx.z * kz, k1 = min(k0 + kz, b.nz);
   const int i = i0 + tx, j = j0 + ty;
   const bool active = (i < b.nx) && (j < b.ny);
@@ -417,6 +417,20 @@ void launch_mu_mode(cudaStream_t s, const KParams &kp, const BlockView &b, const
   const int kz = chunk_z(b.nz, gx * gy, g_mu_slots, 8, true);
   dim3 grd(gx, gy, (b.nz + kz - 1) / kz), blk(TX, TY);
   mu_tiled_kernel<MODE><<<grd, blk, sizeof(MuSmem), s>>>(tm, kp, b, kz);
+}
+
+int mu_tiles_x(int nx) { return (nx + TX - 1) / TX; }
+int mu_tiles_y(int ny) { return (ny + TY - 1) / TY; }
+
+void launch_mu_tiles(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm, int tx0, int tx1,
+                     int ty0, int ty1) {
+  if (tx1 <= tx0 || ty1 <= ty0 || b.nz <= 0) return;
+  BlockView v = b;
+  v.tile_x0 = tx0;
+  v.tile_y0 = ty0;
+  const int kz = chunk_z(b.nz, (tx1 - tx0) * (ty1 - ty0), g_mu_slots, 8, true);
+  dim3 grd(tx1 - tx0, ty1 - ty0, (b.nz + kz - 1) / kz), blk(TX, TY);
+  mu_tiled_kernel<MU_FULL><<<grd, blk, sizeof(MuSmem), s>>>(tm, kp, v, kz);
 }
 
 void launch_mu_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm, int mode) {

@@ -985,7 +985,7 @@ pf_status validate(const pf_grid *g, const pf_params *p) {
       return fail(c, PF_ERR_CONFIG, "%s", why);
   }
   if (p->window && !(p->window_frac > 0 && p->window_frac <= 1)) return fail(c, PF_ERR_CONFIG, "window_frac");
-  if (p->overlap < 0 || p->overlap > 3) return fail(c, PF_ERR_CONFIG, "overlap must be 0..3");
+  if (p->overlap < 0 || p->overlap > 4) return fail(c, PF_ERR_CONFIG, "overlap must be 0..4");
   return PF_OK;
 }
 
@@ -1270,7 +1270,7 @@ pf_status enqueue_step(pf_ctx *c, bool graph) {
   }
   CK(cudaGetLastError());
   const int ov = c->p.overlap;
-  const bool hide_phi = (ov == 2 || ov == 3) && c->p.variant != 1, hide_mu = (ov == 0 || ov == 3) && !graph;
+  const bool hide_phi = (ov == 2 || ov == 3) && c->p.variant != 1, hide_mu = (ov == 0 || ov == 3 || ov == 4) && !graph;
   auto mu_sweep = [&](int mode) -> pf_status {
     TimedSpan ts(c, 1, (int)c->blocks.size());
     for (const auto &b : c->blocks) {
@@ -1282,7 +1282,51 @@ pf_status enqueue_step(pf_ctx *c, bool graph) {
     CK(cudaGetLastError());
     return PF_OK;
   };
-  if (hide_phi) {
+  if (ov == 4 && c->p.variant != 1) {
+    // the phi_dst exchange hidden without Algorithm 2's second pass: the
+    // mu-sweep over the tiles whose stencil reads no ghost (off the x/y block
+    // faces, planes 1 .. nz-2) runs beside it, the shell (the boundary tile
+    // rows / columns, the two cap planes) after it.  Bitwise the cells' values
+    // of the plain mu-sweep (pinned face arithmetic).
+    CK(cudaEventRecord(c->ev_phi_done, c->stream));
+    CK(cudaStreamWaitEvent(c->cstream, c->ev_phi_done, 0));
+    CKS(exchange(c, 0, c->cur ^ 1, true));
+    CK(cudaEventRecord(c->ev_phi_halo, c->cstream));
+    CKS(join_mu(c));
+    {
+      TimedSpan ts(c, 1, (int)c->blocks.size());
+      for (const auto &b : c->blocks) {
+        const int gx = mu_tiles_x(b.nx), gy = mu_tiles_y(b.ny);
+        if (gx >= 3 && gy >= 3 && b.nz >= 3) {
+          launch_mu_tiles(c->stream, c->kp, slab_view(view(c, b, 1), 1, 1, b.nz - 1), maps_of(c, b, 1), 1, gx - 1, 1,
+                          gy - 1);
+          c->launches++;
+        }
+      }
+      CK(cudaGetLastError());
+    }
+    CK(cudaStreamWaitEvent(c->stream, c->ev_phi_halo, 0));
+    {
+      TimedSpan ts(c, 1, (int)c->blocks.size());
+      for (const auto &b : c->blocks) {
+        const int gx = mu_tiles_x(b.nx), gy = mu_tiles_y(b.ny);
+        const BlockView v = view(c, b, 1);
+        if (gx >= 3 && gy >= 3 && b.nz >= 3) {
+          launch_mu_tiles(c->stream, c->kp, v, maps_of(c, b, 1), 0, gx, 0, 1);            // y = 0 row of tiles
+          launch_mu_tiles(c->stream, c->kp, v, maps_of(c, b, 1), 0, gx, gy - 1, gy);      // last row
+          launch_mu_tiles(c->stream, c->kp, v, maps_of(c, b, 1), 0, 1, 1, gy - 1);        // x = 0 column
+          launch_mu_tiles(c->stream, c->kp, v, maps_of(c, b, 1), gx - 1, gx, 1, gy - 1);  // last column
+          launch_mu_tiles(c->stream, c->kp, slab_view(v, 1, 0, 1), maps_of(c, b, 1), 1, gx - 1, 1, gy - 1);
+          launch_mu_tiles(c->stream, c->kp, slab_view(v, 1, b.nz - 1, b.nz), maps_of(c, b, 1), 1, gx - 1, 1, gy - 1);
+          c->launches += 6;
+        } else {
+          launch_mu_tiled(c->stream, c->kp, v, maps_of(c, b, 1), MU_FULL);
+          c->launches++;
+        }
+      }
+      CK(cudaGetLastError());
+    }
+  } else if (hide_phi) {
     // Algorithm 2: phi_dst ghosts on the comm stream while
     // mu-sweep-local (no anti-trapping current: phi_dst needed at the cell
     // only) runs; mu-sweep-neighbor adds the current once the ghosts are in
@@ -1581,6 +1625,14 @@ pf_status pf_set_timing(pf_ctx *c, int32_t on) {
   c->timing = on != 0;
   for (double &m : c->ms) m = 0;
   c->phi_launches = c->mu_launches = 0;
+  return PF_OK;
+}
+
+pf_status pf_set_shortcuts(pf_ctx *c, int32_t on) {
+  CKS(check_state(c, false));
+  c->p.shortcuts = on ? 1 : 0;
+  c->kp.shortcuts = on ? 1 : 0;
+  invalidate_graphs(c);   // the kernel choice and its arguments are captured
   return PF_OK;
 }
 

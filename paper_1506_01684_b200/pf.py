@@ -28,7 +28,8 @@ PF_OK, PF_ERR_CONFIG, PF_ERR_NUMERICAL, PF_ERR_CUDA, PF_ERR_COMM, PF_ERR_STATE, 
 STATUS_NAMES = {0: "PF_OK", -1: "PF_ERR_CONFIG", -2: "PF_ERR_NUMERICAL", -3: "PF_ERR_CUDA", -4: "PF_ERR_COMM",
                 -5: "PF_ERR_STATE", -6: "PF_ERR_ARG", -7: "PF_ERR_IO"}
 EXPORTS = ["pf_nccl_unique_id", "pf_halo_plan", "pf_create", "pf_init", "pf_write", "pf_set_time", "pf_step", "pf_read",
-           "pf_step_io", "pf_save", "pf_load", "pf_mesh", "pf_mesh_table", "pf_set_timing", "pf_info", "pf_last_error", "pf_destroy"]
+           "pf_step_io", "pf_save", "pf_load", "pf_mesh", "pf_mesh_table", "pf_set_timing", "pf_set_shortcuts", "pf_info", "pf_last_error",
+           "pf_destroy"]
 
 
 def mesh_table():
@@ -97,6 +98,7 @@ def lib():
         L.pf_mesh.argtypes = [vp, I32, D, I64, vp, vp, ctypes.POINTER(I64)]
         L.pf_mesh_table.argtypes = [vp]
         L.pf_set_timing.argtypes = [vp, I32]
+        L.pf_set_shortcuts.argtypes = [vp, I32]
         L.pf_info.argtypes = [vp, ctypes.POINTER(PfInfo)]
         L.pf_last_error.argtypes = [vp]
         L.pf_last_error.restype = ctypes.c_char_p
@@ -277,6 +279,10 @@ class Context:
 
     def set_timing(self, on: bool):
         self._check(lib().pf_set_timing(self._c, 1 if on else 0))
+
+    def set_shortcuts(self, on: bool):
+        """Region shortcuts on / off for the following steps (pf_set_shortcuts; bitwise the same results)."""
+        self._check(lib().pf_set_shortcuts(self._c, 1 if on else 0))
 
     def info(self) -> PfInfo:
         o = PfInfo()

@@ -66,3 +66,10 @@ def test_ranks_checkpoint_and_mesh(fakelib):
                layer_height=9.5)
     assert out["equal_phi"] and out["equal_mu"]
     assert out["checkpoint_equal"] and out["mesh_equal"]
+
+
+def test_ranks_interior_shell_mode(fakelib):
+    # overlap mode 4 with blocks large enough to have interior mu tiles (3 x 3
+    # tiles of 32 x 8 per block): the phi halo beside the interior mu-sweep
+    out = _run(fakelib, grid=[192, 48, 24], blocks=[2, 2, 2], steps=6, overlap=4, layer_height=11.5)
+    assert out["equal_phi"] and out["equal_mu"]

@@ -89,3 +89,17 @@ def test_algorithm2_anisotropic_and_window(pv1):
     assert out[0][2] > 0 and out[0][2] == out[1][2] == out[2][2]
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
     assert O.rel_maxnorm(out[0][1], out[2][1]) <= 1e-11
+
+
+@pytest.mark.parametrize("blocks,shape", [((1, 1, 1), (96, 40, 20)), ((2, 2, 2), (192, 48, 24)),
+                                          ((1, 1, 1), (40, 20, 6)), ((2, 1, 1), (70, 9, 12))])
+def test_interior_shell_mode_bitwise(pv1, blocks, shape):
+    # overlap mode 4: the mu-sweep split into the tiles that read no ghost
+    # (beside the hidden phi halo) and the shell after it equals mode 0 bit for
+    # bit — several tile rows / columns, ragged tiles, and blocks too small to
+    # have interior tiles (the plain launch after the halo)
+    nx, ny, nz = shape
+    cfg, (phi, mu) = _state(nx, ny, nz, nz / 2)
+    a = _run(pv1, cfg, phi, mu, 12, 0, blocks=blocks, lh=nz / 2)
+    b = _run(pv1, cfg, phi, mu, 12, 4, blocks=blocks, lh=nz / 2)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])

@@ -166,3 +166,25 @@ def test_interface_dense_state_one_step(pv1):
         ophi, omu = O.step(op, phi, mu)
         assert O.rel_maxnorm(gphi, ophi) <= TOL1
         assert O.rel_maxnorm(gmu, omu) <= TOL1
+
+
+def test_set_shortcuts_toggle_bitwise(pv1):
+    # pf_set_shortcuts switches the region shortcuts between steps: bitwise the
+    # same state as a run without them (C4 recipe, 96x64x80, front moving)
+    pf = _pf()
+    cfg = gen.load_config("c4")
+    spec = gen.spec_from_config(cfg, 96, 64)
+    spec.layer_height, spec.mu_noise = 30.0, 1e-2
+    phi, mu = gen.generate(spec, 96, 64, 80)
+    outs = []
+    for toggle in (False, True):
+        prm = pf.make_params(pv1, cfg, nx=96, ny=64, window=False, layer_height=30.0, T0=pv1["T_eut"] - 0.2)
+        with pf.Context(96, 64, 80, prm) as ctx:
+            ctx.write(phi, mu)
+            ctx.step(10)
+            ctx.set_shortcuts(toggle)
+            ctx.step(20)
+            ctx.set_shortcuts(False)
+            ctx.step(5)
+            outs.append(ctx.read())
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])

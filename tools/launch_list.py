@@ -13,7 +13,7 @@ for r in rows:
         k = k[:k.index("<")].split()[-1] + k[k.index("<"):]
     n, t = agg.get(k, (0, 0.0))
     agg[k] = (n + 1, t + float(r["Metric Value"].replace(",", "")) / 1e6)
-step_k = {k: v for k, v in agg.items() if k.split("<")[0].split()[-1] in
+step_k = {k: v for k, v in agg.items() if k.split("<")[0].split()[-1].split("::")[-1] in
           ("phi_tiled_kernel", "mu_tiled_kernel", "copy_kernel", "table_kernel")}
 tot = sum(t for _, t in step_k.values())
 print(f"# ncu launch list (gpu__time_duration.sum, --clock-control none), {sys.argv[1]}\n")
