@@ -51,6 +51,8 @@ def case(label, name, steps, threads, reps, warm, sweep="step", box=None):
     if sweep == "mu":
         phi1 = O.phi_sweep(p, phi, mu)
         fn = lambda: [O.mu_sweep(p, phi, phi1, mu) for _ in range(steps)]   # noqa: E731
+    elif sweep == "phi":
+        fn = lambda: [O.phi_sweep(p, phi, mu) for _ in range(steps)]   # noqa: E731
     else:
         fn = lambda: O.run(p, phi, mu, steps)   # noqa: E731
     med, ts = timed(fn, reps, warm)
@@ -77,10 +79,19 @@ def main():
         case("C2 full, 10 steps, one core", "c2", 10, 1, R, 0),
         case("C2 mu-sweep alone, 10 sweeps, all cores", "c2", 10, nc, R, 1, sweep="mu"),
         case("C2 mu-sweep alone, 2 sweeps, one core", "c2", 2, 1, R, 1, sweep="mu"),
-        case("C4 512^3, 1 step, all cores", "c4", 1, nc, 1, 0),
-        case("C5 slab 1024x1024x16 at the front, 1 step, all cores", "c5", 1, nc, 1, 0, box=(0, 0, 56, 1024, 1024, 16)),
+        case("C2 phi-sweep alone, 10 sweeps, all cores", "c2", 10, nc, R, 1, sweep="phi"),
+        case("C2 phi-sweep alone, 2 sweeps, one core", "c2", 2, 1, R, 1, sweep="phi"),
+        case("C4 512^3, 10 steps, all cores", "c4", 10, nc, 1, 0),
+        case("C5 slab 1024x1024x256 (the per-GPU share at 4 GPUs), 1 step, all cores", "c5", 1, nc, 1, 0,
+             box=(0, 0, 0, 1024, 1024, 256)),
         case("C5 slab 256x256x16 at the front, 1 step, one core", "c5", 1, 1, 1, 0, box=(0, 0, 56, 256, 256, 16)),
     ]
+    try:
+        ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 1e9
+    except (ValueError, OSError):
+        ram = 0
+    if ram >= 160 and not a.quick:   # the whole 1024^3 state and its successor in host memory (~110 GB)
+        rows.append(case("C5 1024^3, 1 step, all cores", "c5", 1, nc, 1, 0))
     cpu = None
     try:
         for ln in open("/proc/cpuinfo"):
@@ -89,7 +100,11 @@ def main():
                 break
     except OSError:
         pass
-    out = {"host": platform.node(), "cpu": cpu, "nproc": nc,
+    try:
+        mem_gb = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 1e9
+    except (ValueError, OSError):
+        mem_gb = None
+    out = {"host": platform.node(), "cpu": cpu, "nproc": nc, "host_ram_gb": mem_gb,
            "oracle": "oracle/oracle.cpp, g++ -O2 -fno-fast-math -ffp-contract=off -fopenmp (OpenMP over z-planes)",
            "paper_context": "4.2 MLUP/s per SuperMUC Sandy Bridge core, SIMD mu-kernel only (PAPER.md:526)",
            "rows": rows}
