@@ -340,6 +340,7 @@ def run_gpu(args):
         hphi = torch.empty((4,) + shape, dtype=torch.float64, pin_memory=True)
         hmu = torch.empty((2,) + shape, dtype=torch.float64, pin_memory=True)
         ctx.read(hphi, hmu)
+        ctx.step_io(hphi, hmu, hphi, hmu)   # untimed: the slab pipeline's one-time setup (copy lists, streams)
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
