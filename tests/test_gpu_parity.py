@@ -300,8 +300,6 @@ def test_c2_full_one_step(pv1):
 def test_full_size_sampled_one_step(pv1, name, shape):
     nx, ny, nz = shape
     cfg, (phi, mu) = _state(name, nx, ny, nz)
-    if name == "c4":
-        cfg_n = dict(cfg)
     gphi, gmu, _ = _gpu_run(pv1, cfg, phi, mu, 1)
     cells = _sample_cells(nx, ny, nz, 3000)
     # bias the sample towards the front band where all terms are active
@@ -319,6 +317,17 @@ def test_full_size_sampled_one_step(pv1, name, shape):
 # ---------------------------------------------------------------------------
 # NEXT-1 region shortcuts: bitwise identical to the full update
 # ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,shape", [("c4", (512, 512, 512)), ("c5", (1024, 1024, 256))])
+def test_full_size_shortcuts_bitwise(pv1, name, shape):
+    # the region-shortcut kernels at the bench sizes (the skip-faces path over
+    # whole liquid / solid tiles) bitwise against the plain kernels, 3 steps
+    nx, ny, nz = shape
+    cfg, (phi, mu) = _state(name, nx, ny, nz)
+    a = _run_variant(pv1, cfg, phi, mu, 3, False, nx=nx, ny=ny)
+    b = _run_variant(pv1, cfg, phi, mu, 3, True, nx=nx, ny=ny)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
 def _run_variant(pd, cfg, phi, mu, nsteps, shortcuts, blocks=(1, 1, 1), **kw):
     pf = _pf()
     nz, ny, nx = phi.shape[1:]
