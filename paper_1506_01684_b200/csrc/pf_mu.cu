@@ -27,16 +27,25 @@
 
 namespace pf {
 
+#ifndef PF_MU_PM_SLOTS
+#define PF_MU_PM_SLOTS 2
+#endif
+// phi^n / mu tile slots: 2 = staged one plane ahead, 3 = two planes ahead
+// (measured at 512^3: with 32 x 16 tiles, one CTA per SM, the second plane of
+// lead takes C4 from 3.61 to 3.42 ms, still slower than 32 x 8 tiles with one
+// plane of lead, 3.16; 32 x 8 with three slots no longer fits 2 CTAs per SM: 4.74)
+constexpr int NPM = PF_MU_PM_SLOTS;
+
 struct __align__(128) MuSmem {
   double pn[NSLOT][NPH][TSZ];     // phi^{n+1}, planes k-1 .. k+2
-  double po[2][NPH][TSZ];         // phi^n, planes k, k+1
-  double mu[2][NMU][TSZ];         // mu^n,  planes k, k+1
+  double po[NPM][NPH][TSZ];       // phi^n, planes k .. k+NPM-1
+  double mu[NPM][NMU][TSZ];       // mu^n
   double tab[NSLOT][TAB];
   double M[NMU][RY][RX];          // mobility of plane k
   double fx[NMU][TY][TX + 1];     // x-face values at i - 1/2
   double fy[NMU][TY + 1][TX];     // y-face values at j - 1/2
   uint64_t bar_pn[NSLOT];         // phi^{n+1} + table of a plane
-  uint64_t bar_pm[2];             // phi^n + mu of a plane
+  uint64_t bar_pm[NPM];           // phi^n + mu of a plane
   uint32_t wflat[3][NTHR / 32];   // per-warp flatness votes of a staged phi^{n+1}_l plane
 };
 #ifndef PF_MU_UNROLL
@@ -125,8 +134,8 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
 
   auto slot = [&](int k) { return (k - k0 + 1) & (NSLOT - 1); };
   auto par4 = [&](int k) { return (uint32_t)(((k - k0 + 1) >> 2) & 1); };
-  auto slot2 = [&](int k) { return (k - k0) & 1; };
-  auto par2 = [&](int k) { return (uint32_t)(((k - k0) >> 1) & 1); };
+  auto slot2 = [&](int k) { return NPM == 2 ? (k - k0) & 1 : (k - k0) % NPM; };
+  auto par2 = [&](int k) { return (uint32_t)(((k - k0) / NPM) & 1); };
   const int bx = i0 - 2 + XO, by = j0;  // tile box origin (16-byte aligned x)
   auto stage_pn = [&](int k) {            // phi^{n+1} tiles + table row of plane k
     const int s = slot(k);
@@ -197,7 +206,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
   // ---- prologue: phi^{n+1} planes k0-1 .. k0+1, phi^n / mu plane k0
   if (tid == 0) {
     for (int q = 0; q < NSLOT; ++q) mbar_init(&S.bar_pn[q], 1);
-    for (int q = 0; q < 2; ++q) mbar_init(&S.bar_pm[q], 1);
+    for (int q = 0; q < NPM; ++q) mbar_init(&S.bar_pm[q], 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -206,6 +215,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
     stage_pn(k0);
     stage_pn(k0 + 1);
     stage_pm(k0);
+    if (NPM > 2 && k0 + 1 < k1) stage_pm(k0 + 1);
   }
   // Mown: the own column's mobility at plane k, carried from the z-face
   // k-1/2 where it was formed as the upper cell's (same pinned mob2: same bits)
@@ -246,7 +256,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
     // D(k-1), before barrier E(k-1)); own column of plane k+1 into registers
     if (tid == ISSUER) {
       if (k + 2 <= k1) stage_pn(k + 2);
-      if (more) stage_pm(k + 1);
+      if (NPM == 2 ? more : k + NPM - 1 < k1) stage_pm(k + NPM - 1);
     }
     double po_c[NPH], mu_c[NMU];
 #pragma unroll
