@@ -1,8 +1,9 @@
-"""A/B of the mu-sweep kernels (variant 0: per-cell records; 2: the round-1
-tiled kernel) on the C4 state and on the all-guards-open interface state:
-per-sweep CUDA-event times (pf_set_timing), median of the repetitions.
+"""Per-sweep times of a libpf build (PF_LIB selects an A/B copy from
+tools/ab_build.py) on the C4 state and on the all-guards-open interface state
+(the bench's mu_interface measurement): CUDA-event times (pf_set_timing),
+median of the repetitions; --variants picks pf_params.variant (0 tiled, 1 naive).
 
-usage: python tools/mu_ab.py [--n 512] [--reps 5] [--variants 0 2] [--aniso]"""
+usage: [PF_LIB=build/libpf_X.so] python tools/mu_ab.py [--n 512] [--reps 5] [--variants 0] [--aniso]"""
 import argparse
 import json
 import os
@@ -33,7 +34,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=512)
     ap.add_argument("--reps", type=int, default=5)
-    ap.add_argument("--variants", type=int, nargs="+", default=[0, 2])
+    ap.add_argument("--variants", type=int, nargs="+", default=[0])
     ap.add_argument("--tag", default=os.environ.get("PF_LIB", "default"))
     ap.add_argument("--aniso", action="store_true")
     a = ap.parse_args()
