@@ -20,13 +20,23 @@
 
 namespace pf {
 
-struct __align__(128) PhiSmem {
-  double p[NSLOT][NPH][TSZ];       // phi^n tile planes, (row, col) at row * RX + col
-  double tab[NSLOT][TAB];          // per-plane table rows
+#ifndef PF_PHI_NS
+#define PF_PHI_NS 4
+#endif
+// phi^n tile slots: 4 = planes k-1..k+1 resident and k+2 staged at the top of
+// iteration k; 3 = k+2 staged into k-1's slot right after the barrier (with
+// the z-face carry only in the anisotropic layout, the isotropic kernel then
+// fits 5 CTAs per SM at 96 registers: measured 3.68 ms vs 3.55 at 512^3, 3.78
+// at 4 CTAs — the shorter lead costs more than the occupancy gains)
+constexpr int PNS = PF_PHI_NS;
+template <bool ANISO>
+struct __align__(128) PhiSmemT {
+  double p[PNS][NPH][TSZ];         // phi^n tile planes, (row, col) at row * RX + col
+  double tab[PNS][TAB];            // per-plane table rows
   double fx[2][NPH][TY][TX + 1];   // x-face fluxes at i - 1/2, i = 0..TX (plane parity)
   double fy[2][NPH][TY + 1][TX];   // y-face fluxes at j - 1/2, j = 0..TY
-  uint64_t bar[NSLOT];             // one mbarrier per slot
-  double jz[NPH][TY][TX];          // anisotropic: the z-face carry, thread-private (measured: frees
+  uint64_t bar[PNS];               // one mbarrier per slot
+  double jz[ANISO ? NPH : 1][TY][TX];   // anisotropic: the z-face carry, thread-private (measured: frees
                                    // registers the D3C19 faces use; isotropic keeps it in registers)
 };
 
@@ -36,10 +46,13 @@ template <bool ANISO, int SC>   // SC: 0 no shortcut code, 1 the round-1 vote (r
 #ifndef PF_PHI_MINB
 #define PF_PHI_MINB (512 / NTHR)
 #endif
-__global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __grid_constant__ TmaMaps tm, KParams kp, BlockView b,
-                                                            int kz) {
+#ifndef PF_PHI_MINB_ISO
+#define PF_PHI_MINB_ISO PF_PHI_MINB
+#endif
+__global__ void __launch_bounds__(NTHR, ANISO ? PF_PHI_MINB : PF_PHI_MINB_ISO)
+    phi_tiled_kernel(const __grid_constant__ TmaMaps tm, KParams kp, BlockView b, int kz) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  PhiSmem &S = *reinterpret_cast<PhiSmem *>(smem_raw);
+  PhiSmemT<ANISO> &S = *reinterpret_cast<PhiSmemT<ANISO> *>(smem_raw);
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
   const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
   const int k0 = blockIdx.z * kz, k1 = min(k0 + kz, b.nz);
@@ -53,8 +66,8 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
 // 35 % less code, fewer instruction-fetch stalls)
 #define PF_AN (ANISO ? 1 : 0)
 
-  auto slot = [&](int k) { return (k - k0 + 1) & (NSLOT - 1); };
-  auto parity = [&](int k) { return (uint32_t)(((k - k0 + 1) >> 2) & 1); };
+  auto slot = [&](int k) { return PNS == 4 ? (k - k0 + 1) & 3 : (k - k0 + 1) % PNS; };
+  auto parity = [&](int k) { return (uint32_t)(((k - k0 + 1) / PNS) & 1); };
   // plane k -> its slot: 4 phi tiles, 2 mu interior boxes, the table row
   auto stage = [&](int k) {
     const int s = slot(k);
@@ -86,7 +99,7 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
 
   // ---- prologue: planes k0-1, k0, k0+1 resident, z-face k0 - 1/2
   if (tid == 0) {
-    for (int s = 0; s < NSLOT; ++s) mbar_init(&S.bar[s], 1);
+    for (int s = 0; s < PNS; ++s) mbar_init(&S.bar[s], 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -125,7 +138,7 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
   for (int c = 0; c < NMU; ++c) mu_n[c] = active ? __ldg(b.mu[c] + (int64_t)k0 * b.plane + colo) : 0.0;
   for (int k = k0; k < k1; ++k) {
     // A: stage plane k+2 (needed from iteration k+1 on); wait for plane k+1
-    if (tid == ISSUER && k + 2 <= k1) stage(k + 2);
+    if (PNS == 4 && tid == ISSUER && k + 2 <= k1) stage(k + 2);
     double mu_c[NMU];
 #pragma unroll
     for (int c = 0; c < NMU; ++c) {
@@ -303,6 +316,9 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
       for (int a = 0; a < NPH; ++a) q[a] = r0[a] - c * dpart[a];
     }
     __syncthreads();  // B: faces of plane k complete
+    // three slots: plane k+2 into plane k-1's slot, whose last reads (the vote,
+    // the z differences, the anisotropic gradients) came before B(k)
+    if (PNS == 3 && tid == ISSUER && k + 2 <= k1) stage(k + 2);
     if (active && skip) {
       const int64_t o = (int64_t)k * b.plane + colo;
 #pragma unroll
@@ -339,13 +355,13 @@ __global__ void __launch_bounds__(NTHR, PF_PHI_MINB) phi_tiled_kernel(const __gr
 static int g_phi_slots[2] = {1, 1};   // resident CTAs on the GPU, [ANISO]
 
 void prepare_phi_tiled() {
-  const int sm = (int)sizeof(PhiSmem);
-  cudaFuncSetAttribute(phi_tiled_kernel<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(phi_tiled_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(phi_tiled_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(phi_tiled_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  g_phi_slots[0] = grid_slots(phi_tiled_kernel<false, 1>, NTHR, sm);
-  g_phi_slots[1] = grid_slots(phi_tiled_kernel<true, 0>, NTHR, sm);
+  const int sa = (int)sizeof(PhiSmemT<true>), si = (int)sizeof(PhiSmemT<false>);
+  cudaFuncSetAttribute(phi_tiled_kernel<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sa);
+  cudaFuncSetAttribute(phi_tiled_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sa);
+  cudaFuncSetAttribute(phi_tiled_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, si);
+  cudaFuncSetAttribute(phi_tiled_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, si);
+  g_phi_slots[0] = grid_slots(phi_tiled_kernel<false, 1>, NTHR, si);
+  g_phi_slots[1] = grid_slots(phi_tiled_kernel<true, 0>, NTHR, sa);
 }
 
 void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm) {
@@ -355,7 +371,7 @@ void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, con
 #endif
   const int kz = chunk_z(b.nz, gx * gy, g_phi_slots[kp.aniso ? 1 : 0], PF_PHI_WAVES, false);
   dim3 grd(gx, gy, (b.nz + kz - 1) / kz), blk(TX, TY);
-  const size_t sm = sizeof(PhiSmem);
+  const size_t sm = kp.aniso ? sizeof(PhiSmemT<true>) : sizeof(PhiSmemT<false>);
   // shortcuts on: the skip-faces kernels (SC = 2).  Off: the anisotropic kernel
   // without any shortcut code (-3 %), the isotropic one with the round-1
   // run-time check compiled in (its code without it, or with the SC = 2 vote
