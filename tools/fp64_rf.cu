@@ -16,7 +16,9 @@ __global__ void chains(double *out, int iters, double a, double b) {
       for (int c = 0; c < ILP; ++c) {
         if (MODE == 0) x[c] = fma(x[c], a, b);
         else if (MODE == 1) x[c] = fma(x[c], y[c], z[c]);
-        else x[c] = fma(x[c], ys, zs);
+        else if (MODE == 2) x[c] = fma(x[c], ys, zs);
+        else if (MODE == 3) x[c] = x[c] * y[c];
+        else x[c] = x[c] + z[c];
       }
   }
   double s = 0;
@@ -43,6 +45,6 @@ int main() {
   double *out; cudaMalloc(&out, 8);
   run<1, 0>(nsm, out); run<1, 1>(nsm, out); run<1, 2>(nsm, out);
   run<2, 0>(nsm, out); run<2, 1>(nsm, out); run<2, 2>(nsm, out);
-  run<4, 0>(nsm, out); run<4, 1>(nsm, out); run<4, 2>(nsm, out);
+  run<4, 0>(nsm, out); run<4, 1>(nsm, out); run<4, 2>(nsm, out); run<4, 3>(nsm, out); run<4, 4>(nsm, out);
   return 0;
 }
