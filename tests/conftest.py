@@ -23,3 +23,9 @@ def pv1():
 def psym():
     from inputs import gen
     return gen.load_params("sym")
+
+
+@pytest.fixture(scope="session")
+def pgen():
+    from inputs import gen
+    return gen.load_params("generic")

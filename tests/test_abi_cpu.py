@@ -116,3 +116,18 @@ def test_create_rejects_unstable_dt_and_nonpositive_A():
     with pytest.raises(pf.PfError) as e:
         pf.Context(8, 8, 8, prm)
     assert e.value.status == pf.PF_ERR_CONFIG and "<= 0" in str(e.value), str(e.value)
+
+
+def test_generic_params_pass_validation():
+    # params/generic.json (distinct coefficients, tests/test_gpu_generic.py) is
+    # inside the explicit-Euler bound and keeps A(T) > 0: pf_create's
+    # validation accepts it, isotropic and with the full anisotropy matrix
+    from paper_1506_01684_b200 import pf
+    from inputs import gen
+    cfg = gen.load_config("c2")
+    for aniso in (False, True):
+        prm = pf.make_params(gen.load_params("generic"), cfg, aniso=aniso)
+        try:
+            pf.Context(40, 19, 12, prm).close()
+        except pf.PfError as e:   # no GPU here: validation passed, the device step failed
+            assert e.status == pf.PF_ERR_CUDA, str(e)

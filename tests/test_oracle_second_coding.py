@@ -74,3 +74,44 @@ def test_unequal_mobilities_agree(pv1, aniso):
     b = ON.step(p, phi, mu, n=1, zorig=0)
     assert O.rel_maxnorm(b[0], a[0]) <= TOL1
     assert O.rel_maxnorm(b[1], a[1]) <= TOL1
+
+
+def _generic(pd, aniso, **over):
+    # the full per-pair delta matrix of PARAMS-generic (no delta_sl override)
+    return O.make_params(dict(pd, **over), layer_height=3.0, aniso=aniso, delta_sl=None)
+
+
+@pytest.mark.parametrize("kind", ["random", "triple", "binary"])
+@pytest.mark.parametrize("aniso", [False, True])
+def test_generic_parameters_agree(pgen, kind, aniso):
+    # every per-phase / per-pair / per-triple coefficient distinct (params/generic.json):
+    # a transposed pair index, a triple taken from the wrong phase or a solid's
+    # coefficient read for another solid changes the result in one coding only
+    phi, mu = crafted(kind, 8, 8, 8, seed=11)
+    p = _generic(pgen, aniso, G=0.02, v=0.5)
+    a = O.step(p, phi, mu, n=4, zorig=2)
+    b = ON.step(p, phi, mu, n=4, zorig=2)
+    assert O.rel_maxnorm(b[0], a[0]) <= TOL1
+    assert O.rel_maxnorm(b[1], a[1]) <= TOL1
+    assert np.abs(a[0] - phi).max() > 1e-4 and np.abs(a[1] - mu).max() > 1e-4
+
+
+def test_generic_parameters_matter(pgen, pv1):
+    # the generic set is not a relabelling of v1: both codings move away from v1's result
+    phi, mu = crafted("random", 8, 8, 8, seed=11)
+    a = O.step(_generic(pgen, True, G=0.02, v=0.5), phi, mu, n=4, zorig=2)
+    v = O.step(_params(pv1, True, G=0.02, v=0.5), phi, mu, n=4, zorig=2)
+    assert np.abs(a[0] - v[0]).max() > 1e-4 and np.abs(a[1] - v[1]).max() > 1e-4
+
+
+@pytest.mark.parametrize("aniso", [False, True])
+def test_generic_trajectory_agrees(pgen, aniso):
+    cfg = gen.load_config("c2")
+    spec = gen.spec_from_config(cfg, 12, 10)
+    spec.n_seeds, spec.layer_height, spec.mu_noise = 5, 4.0, 5e-2
+    phi, mu = gen.generate(spec, 12, 10, 8)
+    p = _generic(pgen, aniso, G=0.02, v=0.5)
+    a = O.run(p, phi, mu, 20)
+    b = ON.run(p, phi, mu, 20)
+    assert O.rel_maxnorm(b[0], a[0]) <= TOLN
+    assert O.rel_maxnorm(b[1], a[1]) <= TOLN

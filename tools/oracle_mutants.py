@@ -63,6 +63,21 @@ MUTANTS = [
      "* pd * dot * na[d];", "* pd * dot * nl[d];"),
     ("diffusive flux with the harmonic instead of the arithmetic mobility (reading R11)",
      "F[c] = (lo.M[c] + hi.M[c]) / R(2.0)", "F[c] = (lo.M[c] * hi.M[c]) / R(2.0)"),
+    # index slips: visible only with distinct per-phase / per-pair coefficients (params/generic.json)
+    ("triple coefficient of the wrong triple in d omega (O4.7)",
+     "s = s + R(p.gamma3[x]) * ph[b] * ph[e];", "s = s + R(p.gamma3[a]) * ph[b] * ph[e];"),
+    ("pair coefficient gamma_ab read as gamma_a,l in d omega (O4.7)",
+     "if (b != a) s = s + R(16.0 / (M_PI * M_PI) * p.gamma[a][b]) * ph[b];",
+     "if (b != a) s = s + R(16.0 / (M_PI * M_PI) * p.gamma[a][N - 1 - (a == N - 1)]) * ph[b];"),
+    ("anisotropy strength of the solid-liquid pair for every pair (O4.3)",
+     "const R ac = R(1.0) - R(p.delta[a][b]) * (R(3.0) - R(4.0) * Q4 / q4);",
+     "const R ac = R(1.0) - R(p.delta[a][N - 1 - (a == N - 1)]) * (R(3.0) - R(4.0) * Q4 / q4);"),
+    ("relaxation time tau of phase 0 for every phase (Eq. 1)",
+     "R(p.dt / (p.tau[a] * p.eps))", "R(p.dt / (p.tau[0] * p.eps))"),
+    ("mobility D of component 0 for both components (O5.6)",
+     "q.po[a] * R(p.D[a][c] / (2.0 * A_of(p, a, c, T)))", "q.po[a] * R(p.D[a][0] / (2.0 * A_of(p, a, c, T)))"),
+    ("A1 of component 0 in the kappa term of dc/dT (O5.5)",
+     "q.mu[c] * R(2.0 * p.A1[a][c] / (twoA * twoA))", "q.mu[c] * R(2.0 * p.A1[a][0] / (twoA * twoA))"),
     ("projection threshold from rho+1 terms (O4.11)",
      "if (val(u[jdx]) - val(t) > 0.0) theta = t;", "if (val(u[jdx]) - val(t) >= 0.0) theta = t + R(1e-3);"),
 ]
