@@ -503,24 +503,12 @@ __device__ __forceinline__ double mu_flux_diff(const KParams &kp, double Mlo, do
 // and of the live temporaries; only for accessors whose operands are in
 // shared memory — an operand array in registers indexed by a run-time solid
 // would be put in local memory)
+// exact-zero guards as integer tests on the bits (is_zero_bits)
+#define PF_ZERO(x) is_zero_bits(x)
 template <bool DIFF = true, bool ROLL = false, class QL, class QH>
 __device__ __forceinline__ void mu_face_t(const KParams &kp, const QL &lo, const QH &hi, int d, double out[NMU]) {
 #pragma unroll
   for (int c = 0; c < NMU; ++c) out[c] = DIFF ? mu_flux_diff(kp, lo.M(c), hi.M(c), lo.mu(c), hi.mu(c)) : 0.0;
-#ifndef PF_MU_RCPNR
-#define PF_MU_RCPNR 1
-#endif
-#ifndef PF_MU_INTZ
-#define PF_MU_INTZ 1
-#endif
-#ifndef PF_MU_HOIST
-#define PF_MU_HOIST 1
-#endif
-#if PF_MU_INTZ
-#define PF_ZERO(x) is_zero_bits(x)
-#else
-#define PF_ZERO(x) ((x) == 0.0)
-#endif
   const double sl = RN_ADD(lo.pn(LIQ), hi.pn(LIQ));
   if (PF_ZERO(sl)) return;                  // no liquid: J = 0 (bulk solid exits here)
   // gradient components in the order (normal d, tangential d+1, d+2) — scalars,
@@ -537,19 +525,13 @@ __device__ __forceinline__ void mu_face_t(const KParams &kp, const QL &lo, const
     for (int a = 0; a < 3; ++a) sa[a] = RN_ADD(lo.pn(a), hi.pn(a));
     S = RN_FMA(sa[2], sa[2], RN_FMA(sa[1], sa[1], RN_FMA(sa[0], sa[0], S)));
   }
-#if PF_MU_RCPNR
   const double rS = exp_outside(S, 1000) ? __drcp_rn(S) : rcp_nr(S);   // rcp.approx flushes subnormals
-#else
-  const double rS = __drcp_rn(S);
-#endif
   // (pi eps / 16 dt) h_l
   const double khl = RN_MUL(kp.pi_eps_16dt, RN_MUL(RN_MUL(sl, sl), rS));
   // x / y faces: both cells share the plane's table row, so the (c^l - c^a)
   // sum is (mu_lo + mu_hi) (1/2A^l - 1/2A^a) + 2 (chat^l - chat^a); a z face's
   // cells each use their own plane's row
-#if PF_MU_HOIST
   const double ms0 = RN_ADD(lo.mu(0), hi.mu(0)), ms1 = RN_ADD(lo.mu(1), hi.mu(1));
-#endif
   double J0 = 0.0, J1 = 0.0;
   auto solid = [&](int a) {
     const double saa = RN_ADD(lo.pn(a), hi.pn(a));
@@ -572,13 +554,8 @@ __device__ __forceinline__ void mu_face_t(const KParams &kp, const QL &lo, const
     double dc0, dc1;
     if (d < 2) {
       const double *t = lo.tab();
-#if PF_MU_HOIST
       dc0 = RN_FMA(ms0, t[T_DI2A + a * 2], t[T_DCHAT2 + a * 2]);
       dc1 = RN_FMA(ms1, t[T_DI2A + a * 2 + 1], t[T_DCHAT2 + a * 2 + 1]);
-#else
-      dc0 = RN_FMA(RN_ADD(lo.mu(0), hi.mu(0)), t[T_DI2A + a * 2], t[T_DCHAT2 + a * 2]);
-      dc1 = RN_FMA(RN_ADD(lo.mu(1), hi.mu(1)), t[T_DI2A + a * 2 + 1], t[T_DCHAT2 + a * 2 + 1]);
-#endif
     } else {
       dc0 = RN_ADD(lo.dcl(a, 0), hi.dcl(a, 0));
       dc1 = RN_ADD(lo.dcl(a, 1), hi.dcl(a, 1));
