@@ -127,6 +127,8 @@ enum {
   T_DI2A = 48,    // 1/(2A^l) - 1/(2A^a), solids a < 3
   T_DCHAT = 54,   // chat^l - chat^a,     solids a < 3
   T_DCHAT2 = 60,  // 2 (chat^l - chat^a): the x/y-face sum of (c^l - c^a) (mu_face_t)
+  T_EPSTDX16 = 66,   // eps T / (16 dx^2): the divergence factor of the anisotropic face fluxes,
+                     // which phi_face returns scaled by 16 dx
   TAB = 68        // multiple of 4 doubles (32 B): rows stay aligned
 };
 static_assert(TAB % 4 == 0, "table row alignment");
@@ -147,7 +149,8 @@ __device__ __forceinline__ double2 tab2(const double *__restrict__ tab, int base
 //
 // g is homogeneous of degree 1; the direct formula needs |q|^-4 and Q4, which
 // leave the double range for |q| < ~1e-77.  Below |q|^2 = 2^-400 (|q| <
-// 1.5e-60) g is returned as 0 — an absolute error under 1e-59 (DESIGN.md
+// 1.5e-60 of the vector passed in: the sweeps pass 8 dx q at faces, 2 dx q in
+// the cell update) g is returned as 0 — an absolute error under 1e-59 (DESIGN.md
 // reading R30; the oracle evaluates those exactly by power-of-two scaling).
 // The test is an integer compare on |q|^2's exponent and an early return, the
 // round-1 exit for q = 0 (absent pairs: most pairs of a bulk cell) widened —
@@ -227,47 +230,51 @@ __device__ __forceinline__ void phi_face(const KParams &kp, const double plo[NPH
       jf[b] = RN_FMA(G, s[a], jf[b]);
     }
   } else {
-    double pb[NPH], gn[NPH];
+    // anisotropic, on raw differences: glo / ghi are the cells' raw centre
+    // differences phi(c+e) - phi(c-e) (= 2 dx grad), so with the face sums
+    // s = lo + hi (= 2 phibar), the normal 4 (hi - lo) and the tangential sums
+    // glo + ghi (both = 4 dx grad phi at the face) the pair vector is
+    // q' = s_a G_b - s_b G_a = 8 dx q; g is homogeneous of degree 1 in q
+    // (pin P21), so the returned flux is 16 dx j_a (divergence factor
+    // T_EPSTDX16) — no 1/2, 1/dx or 1/(2dx) per operand
+    double s[NPH], gn[NPH];
 #pragma unroll
     for (int a = 0; a < NPH; ++a) {
-      pb[a] = RN_MUL(0.5, RN_ADD(plo[a], phi_[a]));
-      gn[a] = RN_MUL(RN_SUB(phi_[a], plo[a]), kp.inv_dx);
+      s[a] = RN_ADD(plo[a], phi_[a]);
+      gn[a] = RN_MUL(4.0, RN_SUB(phi_[a], plo[a]));
     }
     double gf[NPH][3];
 #pragma unroll
     for (int a = 0; a < NPH; ++a)
 #pragma unroll
       for (int e = 0; e < 3; ++e)
-        gf[a][e] = (e == d) ? gn[a] : RN_MUL(0.5, RN_ADD(glo[a][e], ghi[a][e]));
+        gf[a][e] = (e == d) ? gn[a] : RN_ADD(glo[a][e], ghi[a][e]);
 #pragma unroll
     for (int p = 0; p < 6; ++p) {
       const int a = pair_a(p), b = pair_b(p);
       double q[3];
 #pragma unroll
-      for (int e = 0; e < 3; ++e) q[e] = RN_FMA(pb[a], gf[b][e], -RN_MUL(pb[b], gf[a][e]));
+      for (int e = 0; e < 3; ++e) q[e] = RN_FMA(s[a], gf[b][e], -RN_MUL(s[b], gf[a][e]));
       // only the normal component g_d of the pair gradient enters the flux
       const double gd = kp.delta[p] == 0.0 ? RN_MUL(kp.g2[p], q[d]) : pair_grad_aniso_d(kp.g2[p], kp.delta[p], q, d);
-      jf[a] = RN_FMA(-gd, pb[b], jf[a]);
-      jf[b] = RN_FMA(gd, pb[a], jf[b]);
+      jf[a] = RN_FMA(-gd, s[b], jf[a]);
+      jf[b] = RN_FMA(gd, s[a], jf[b]);
     }
   }
 }
 
-// Raw centre difference hi - lo (the mu-sweep's anti-trapping gradients, which
-// are scale-free), pinned.
+// Raw centre difference hi - lo (2 dx times the centre gradient: the phi-sweep's
+// and the anti-trapping current's gradients, which fold the 1/(2 dx) into
+// their constants), pinned.
 __device__ __forceinline__ double cdiff(double lo, double hi) { return RN_SUB(hi, lo); }
 
-// Centre gradient (hi - lo) / (2 dx), pinned.
-__device__ __forceinline__ double cgrad(const KParams &kp, double lo, double hi) {
-  return RN_MUL(RN_SUB(hi, lo), kp.inv_2dx);
-}
 
 // Cell part of the phi update (oracle O4.1-4.11) given the cell value, its
 // chemical potential, centre gradients, the face-flux divergence sum_d (j^+ -
-// j^-) (before the 1/dx factor) and the plane's table row.  Isotropic runs
-// pass the raw centre differences phi(c+e) - phi(c-e) instead of the
-// gradients: there they only enter the Gram matrix, whose 1/(2dx)^2 is folded
-// into g2mc.
+// j^-) (before the 1/dx factor) and the plane's table row.  Both models take
+// the raw centre differences phi(c+e) - phi(c-e) instead of the gradients:
+// they enter the Gram matrix (isotropic) or the pair vectors (anisotropic,
+// g homogeneous of degree 1) quadratically, the 1/(2dx)^2 folded into g2c.
 // Split in two so the tiled sweep can do everything that does not need the
 // face fluxes before its CTA barrier: phi_cell_rhs0 returns
 // r0_a = eps T da/dphi_a + (T/eps) domega/dphi_a + dpsi/dphi_a (O4.2-4.4,
@@ -337,11 +344,13 @@ __device__ __forceinline__ void phi_cell_rhs0(const KParams &kp, const double *_
       double q[3], g[3];
 #pragma unroll
       for (int e = 0; e < 3; ++e) q[e] = ph[a] * gc[b][e] - ph[b] * gc[a][e];
+      // raw centre differences (2 dx grad): q is 2 dx too large, g (degree 1)
+      // as well, dad by (2 dx)^2 — g2c carries the 1/(2 dx)^2
       if (kp.delta[p] != 0.0) {
-        pair_grad_aniso(kp.g2[p], kp.delta[p], q, g);
+        pair_grad_aniso(kp.g2c[p], kp.delta[p], q, g);
       } else {
 #pragma unroll
-        for (int e = 0; e < 3; ++e) g[e] = kp.g2[p] * q[e];
+        for (int e = 0; e < 3; ++e) g[e] = kp.g2c[p] * q[e];
       }
       dad[a] += g[0] * gc[b][0] + g[1] * gc[b][1] + g[2] * gc[b][2];
       dad[b] -= g[0] * gc[a][0] + g[1] * gc[a][1] + g[2] * gc[a][2];
@@ -389,8 +398,9 @@ __device__ __forceinline__ void phi_cell_rhs0(const KParams &kp, const double *_
 __device__ __forceinline__ void phi_cell_finish(const KParams &kp, const double *__restrict__ tab,
                                                 const double ph[NPH], const double r0[NPH],
                                                 const double dsum[NPH], double out[NPH]) {
-  // O4.9 with the O4.6 divergence of the face fluxes (eps T / dx folded)
-  const double epsTdx = tab[T_EPSTDX];
+  // O4.9 with the O4.6 divergence of the face fluxes (eps T / dx folded; the
+  // anisotropic fluxes come scaled by 16 dx)
+  const double epsTdx = tab[kp.aniso ? T_EPSTDX16 : T_EPSTDX];
   double rhs[NPH];
 #pragma unroll
   for (int a = 0; a < NPH; ++a) rhs[a] = r0[a] - epsTdx * dsum[a];

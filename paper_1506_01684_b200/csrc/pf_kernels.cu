@@ -25,6 +25,7 @@ __global__ void table_kernel(double *tab, int64_t nplanes, TabParams tp, int64_t
   row[T_EPST] = tp.eps * T;
   row[T_TEPS] = T / tp.eps;
   row[T_EPSTDX] = tp.eps * T / tp.dx;
+  row[T_EPSTDX16] = tp.eps * T / (16.0 * tp.dx * tp.dx);
   for (int a = 0; a < NPH; ++a) {
     row[T_B + a] = tp.L[a] * th / tp.T_eut;
     for (int c = 0; c < NMU; ++c) {
@@ -63,15 +64,16 @@ __device__ __forceinline__ void load_phi(const BlockView &b, int64_t o, double v
   for (int a = 0; a < NPH; ++a) v[a] = __ldg(b.phi[a] + o);
 }
 
-// centre gradients of all phases; component `skip` (the face normal of a
+// raw centre differences phi(c+e) - phi(c-e) of all phases (the convention of
+// phi_face and phi_cell_rhs0); component `skip` (the face normal of a
 // neighbour cell, never used) is set to 0 instead of reading 2 cells away.
-__device__ __forceinline__ void centre_grads(const KParams &kp, const double *const f[NPH], int64_t o,
-                                             const int64_t st[3], double g[NPH][3], int skip = -1) {
+__device__ __forceinline__ void centre_diffs(const double *const f[NPH], int64_t o, const int64_t st[3],
+                                             double g[NPH][3], int skip = -1) {
 #pragma unroll
   for (int e = 0; e < 3; ++e)
 #pragma unroll
     for (int a = 0; a < NPH; ++a)
-      g[a][e] = (e == skip) ? 0.0 : cgrad(kp, __ldg(f[a] + o - st[e]), __ldg(f[a] + o + st[e]));
+      g[a][e] = (e == skip) ? 0.0 : cdiff(__ldg(f[a] + o - st[e]), __ldg(f[a] + o + st[e]));
 }
 
 __global__ void __launch_bounds__(128) phi_naive_kernel(KParams kp, BlockView b) {
@@ -85,25 +87,20 @@ __global__ void __launch_bounds__(128) phi_naive_kernel(KParams kp, BlockView b)
   load_phi(b, o, ph);
   mu[0] = __ldg(b.mu[0] + o);
   mu[1] = __ldg(b.mu[1] + o);
-  centre_grads(kp, b.phi, o, st, gc);
-  double gcu[NPH][3];   // phi_cell_update: raw centre differences when isotropic
-#pragma unroll
-  for (int a = 0; a < NPH; ++a)
-#pragma unroll
-    for (int e = 0; e < 3; ++e) gcu[a][e] = kp.aniso ? gc[a][e] : __ldg(b.phi[a] + o + st[e]) - __ldg(b.phi[a] + o - st[e]);
+  centre_diffs(b.phi, o, st, gc);
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     double pl[NPH], pu[NPH], gl[NPH][3], gu[NPH][3];
     load_phi(b, o - st[d], pl);
     load_phi(b, o + st[d], pu);
     if (kp.aniso) {
-      centre_grads(kp, b.phi, o - st[d], st, gl, d);
-      centre_grads(kp, b.phi, o + st[d], st, gu, d);
+      centre_diffs(b.phi, o - st[d], st, gl, d);
+      centre_diffs(b.phi, o + st[d], st, gu, d);
     }
     phi_face(kp, pl, ph, gl, gc, d, jm[d]);
     phi_face(kp, ph, pu, gc, gu, d, jp[d]);
   }
-  phi_cell_update(kp, b.tab + (int64_t)k * TAB, ph, mu, gcu, jm, jp, out);
+  phi_cell_update(kp, b.tab + (int64_t)k * TAB, ph, mu, gc, jm, jp, out);
 #pragma unroll
   for (int a = 0; a < NPH; ++a) b.out[a][o] = out[a];
 }

@@ -81,14 +81,14 @@ __global__ void __launch_bounds__(NTHR, ANISO ? PF_PHI_MINB : PF_PHI_MINB_ISO)
     bulk_load(S.tab[s], b.tab + (int64_t)k * TAB, TAB * 8, &S.bar[s]);
   };
   auto wait = [&](int k) { mbar_wait(&S.bar[slot(k)], parity(k)); };
-  // tangential centre gradients of tile cell (col,row) in slot sc (component
-  // d unused); z-tangential from slots sm/sp
+  // tangential raw centre differences of tile cell (col,row) in slot sc
+  // (component d unused); z-tangential from slots sm/sp
   auto tan_grad = [&](int sc, int sm, int sp, int col, int row, int d, double g[NPH][3]) {
 #pragma unroll
     for (int a = 0; a < NPH; ++a) {
-      g[a][0] = d == 0 ? 0.0 : cgrad(kp, T(S.p[sc][a], row, col - 1), T(S.p[sc][a], row, col + 1));
-      g[a][1] = d == 1 ? 0.0 : cgrad(kp, T(S.p[sc][a], row - 1, col), T(S.p[sc][a], row + 1, col));
-      g[a][2] = d == 2 ? 0.0 : cgrad(kp, T(S.p[sm][a], row, col), T(S.p[sp][a], row, col));
+      g[a][0] = d == 0 ? 0.0 : cdiff(T(S.p[sc][a], row, col - 1), T(S.p[sc][a], row, col + 1));
+      g[a][1] = d == 1 ? 0.0 : cdiff(T(S.p[sc][a], row - 1, col), T(S.p[sc][a], row + 1, col));
+      g[a][2] = d == 2 ? 0.0 : cdiff(T(S.p[sm][a], row, col), T(S.p[sp][a], row, col));
     }
   };
   double gdum[NPH][3];
@@ -192,8 +192,8 @@ __global__ void __launch_bounds__(NTHR, ANISO ? PF_PHI_MINB : PF_PHI_MINB_ISO)
     if (!ANISO)
 #pragma unroll
       for (int a = 0; a < NPH; ++a) pc[a] = T(S.p[sc][a], orow, oc);
-    // anisotropic: the own cell's centre gradients once (the hi side of its
-    // -x / -y faces and the cell update's gradients; pinned cgrad: same bits)
+    // anisotropic: the own cell's raw centre differences once (the hi side of
+    // its -x / -y faces and the cell update's gradients; pinned: same bits)
     double gown[NPH][3];
     if (ANISO) tan_grad(sc, sm, sp, oc, orow, -1, gown);
     {
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(NTHR, ANISO ? PF_PHI_MINB : PF_PHI_MINB_ISO)
 #pragma unroll
       for (int a = 0; a < NPH; ++a) b.out[a][o] = pc[a];
     } else if (active) {
-      const double c = S.tab[sc][T_EPSTDX];
+      const double c = S.tab[sc][ANISO ? T_EPSTDX16 : T_EPSTDX];   // anisotropic fluxes: 16 dx j
       if (ANISO) {
         double r0[NPH];
         phi_cell_rhs0<PF_AN>(kp, S.tab[sc], pc, mu_c, gown, r0);
