@@ -51,6 +51,8 @@ struct KParams {
   double Gv;               // G v = -dT/dt
   int aniso;
   int shortcuts;           // region shortcuts (NEXT-1): skip the phi update of bulk warps
+  int dmask;               // bit p set: delta of pair p is not 0 (the cubic g applies)
+  int pad1_;
 };
 
 // 1/s to within an ulp (faithful, not correctly rounded): the hardware
@@ -170,7 +172,7 @@ __device__ __forceinline__ void pair_grad_aniso(double g2, double delta, const d
 #pragma unroll
   for (int d = 0; d < 3; ++d) { s2[d] = RN_MUL(q[d], q[d]); }
   s4 = RN_FMA(s2[2], s2[2], RN_FMA(s2[1], s2[1], RN_MUL(s2[0], s2[0])));   // Q4
-  const double r2 = __drcp_rn(q2);
+  const double r2 = rcp_nr(q2);   // q2 >= 2^-400: normal, no IEEE special cases (measured -6 % aniso phi)
   const double r4 = RN_MUL(r2, r2);
   const double x = RN_MUL(s4, r4);                                          // Q4/|q|^4
   const double ac = RN_SUB(1.0, RN_MUL(delta, RN_FMA(-4.0, x, 3.0)));       // a_c
@@ -192,7 +194,7 @@ __device__ __forceinline__ double pair_grad_aniso_d(double g2, double delta, con
 #pragma unroll
   for (int e = 0; e < 3; ++e) s2[e] = RN_MUL(q[e], q[e]);
   const double s4 = RN_FMA(s2[2], s2[2], RN_FMA(s2[1], s2[1], RN_MUL(s2[0], s2[0])));
-  const double r2 = __drcp_rn(q2);
+  const double r2 = rcp_nr(q2);   // q2 >= 2^-400: normal, no IEEE special cases (measured -6 % aniso phi)
   const double r4 = RN_MUL(r2, r2);
   const double x = RN_MUL(s4, r4);
   const double ac = RN_SUB(1.0, RN_MUL(delta, RN_FMA(-4.0, x, 3.0)));
@@ -256,7 +258,7 @@ __device__ __forceinline__ void phi_face(const KParams &kp, const double plo[NPH
 #pragma unroll
       for (int e = 0; e < 3; ++e) q[e] = RN_FMA(s[a], gf[b][e], -RN_MUL(s[b], gf[a][e]));
       // only the normal component g_d of the pair gradient enters the flux
-      const double gd = kp.delta[p] == 0.0 ? RN_MUL(kp.g2[p], q[d]) : pair_grad_aniso_d(kp.g2[p], kp.delta[p], q, d);
+      const double gd = !((kp.dmask >> p) & 1) ? RN_MUL(kp.g2[p], q[d]) : pair_grad_aniso_d(kp.g2[p], kp.delta[p], q, d);
       jf[a] = RN_FMA(-gd, s[b], jf[a]);
       jf[b] = RN_FMA(gd, s[a], jf[b]);
     }
@@ -346,7 +348,7 @@ __device__ __forceinline__ void phi_cell_rhs0(const KParams &kp, const double *_
       for (int e = 0; e < 3; ++e) q[e] = ph[a] * gc[b][e] - ph[b] * gc[a][e];
       // raw centre differences (2 dx grad): q is 2 dx too large, g (degree 1)
       // as well, dad by (2 dx)^2 — g2c carries the 1/(2 dx)^2
-      if (kp.delta[p] != 0.0) {
+      if ((kp.dmask >> p) & 1) {
         pair_grad_aniso(kp.g2c[p], kp.delta[p], q, g);
       } else {
 #pragma unroll

@@ -1061,6 +1061,8 @@ pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
     kp.omp[q] = 16.0 / (M_PI * M_PI) * p->gamma[pair_a(q)][pair_b(q)];
     kp.delta[q] = p->aniso ? p->delta[pair_a(q)][pair_b(q)] : 0.0;
   }
+  kp.dmask = 0;
+  for (int q = 0; q < 6; ++q) kp.dmask |= (kp.delta[q] != 0.0 ? 1 : 0) << q;
   kp.pi_eps_16dt = M_PI * p->eps / (16.0 * p->dt);
   kp.Gv = p->G * p->v;
   kp.aniso = p->aniso ? 1 : 0;
