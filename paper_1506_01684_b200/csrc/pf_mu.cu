@@ -49,7 +49,7 @@ struct __align__(128) MuSmem {
   uint32_t wflat[3][NTHR / 32];   // per-warp flatness votes of a staged phi^{n+1}_l plane
 };
 #ifndef PF_MU_UNROLL
-#define PF_MU_UNROLL 2
+#define PF_MU_UNROLL 4
 #endif
 #ifndef PF_MU_ROLL
 #define PF_MU_ROLL 1
@@ -59,7 +59,9 @@ struct __align__(128) MuSmem {
 // code (measured on the all-guards-open state: 13.6 -> 10.8 ms; C4 unchanged)
 constexpr bool kMuRoll = PF_MU_ROLL != 0;
 constexpr int kMuUnroll = PF_MU_UNROLL;   // plane-loop unroll (round 1: 2 -> 4 -0.8 %; with the rolled anti-trapping
-                                          // solids 4 costs registers: C4 3.78 vs 3.15 ms, interface 11.8 vs 11.2 ms)
+                                          // solids and the library-call fallback, 4 spilled: C4 3.78 vs 3.15 ms; without
+                                          // the fallback (R31): 4 vs 2 C4 3.104 vs 3.127, interface 9.97 vs 10.39;
+                                          // 3: 3.129 / 10.46, 8: 3.46 / 11.5; 4 unrolled solids: 3.161 / 9.48)
 constexpr int NBOX = RX * RY;     // staged cells of a plane tile (interior + ring + corners)
 static_assert(NBOX <= 2 * NTHR, "flatness check covers the box in two passes");
 #define T(arr, row, col) TILE_AT(arr, row, col)
