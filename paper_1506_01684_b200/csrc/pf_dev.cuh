@@ -369,7 +369,9 @@ __device__ __forceinline__ void phi_cell_rhs0(const KParams &kp, const double *_
     ps[a] = s;
   }
   const double S = ph[0] * ph[0] + ph[1] * ph[1] + ph[2] * ph[2] + ph[3] * ph[3];
-  const double rS = 1.0 / S;   // (rcp_nr here measured +0.7 %: the FP64 pipe, not latency, binds)
+  // S in [1/4, 1] on simplex states.  The faithful reciprocal measured -0.4 % in
+  // the anisotropic kernel and +0.9 % in the isotropic one (register allocation)
+  const double rS = AN == 1 ? rcp_nr(S) : 1.0 / S;
   const double pbar = rS * (ph[0] * ph[0] * ps[0] + ph[1] * ph[1] * ps[1] + ph[2] * ph[2] * ps[2] +
                             ph[3] * ph[3] * ps[3]);
   const double epsT = tab[T_EPST], Teps = tab[T_TEPS];
