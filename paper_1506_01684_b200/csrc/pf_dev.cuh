@@ -209,7 +209,10 @@ __device__ __forceinline__ double pair_grad_aniso_d(double g2, double delta, con
 // j_a = -sum_{b != a} g_ab,d(q_ab) phibar_b.  Pinned rounding.
 // AN: -1 = the model from kp.aniso at run time, 0 / 1 = isotropic / anisotropic
 // fixed at compile time (the tiled sweep's two kernels carry only their own code)
-template <int AN = -1>
+// DM: the cubic pairs' mask (bit p: delta_p != 0) fixed at compile time, or -1
+// for kp.dmask at run time (the anisotropic sweep instantiates the solid-liquid
+// case, C5's model, without the per-pair branch)
+template <int AN = -1, int DM = -1>
 __device__ __forceinline__ void phi_face(const KParams &kp, const double plo[NPH], const double phi_[NPH],
                                          const double glo[NPH][3], const double ghi[NPH][3], int d,
                                          double jf[NPH]) {
@@ -258,7 +261,8 @@ __device__ __forceinline__ void phi_face(const KParams &kp, const double plo[NPH
 #pragma unroll
       for (int e = 0; e < 3; ++e) q[e] = RN_FMA(s[a], gf[b][e], -RN_MUL(s[b], gf[a][e]));
       // only the normal component g_d of the pair gradient enters the flux
-      const double gd = !((kp.dmask >> p) & 1) ? RN_MUL(kp.g2[p], q[d]) : pair_grad_aniso_d(kp.g2[p], kp.delta[p], q, d);
+      const bool cubic = DM < 0 ? ((kp.dmask >> p) & 1) != 0 : ((DM >> p) & 1) != 0;
+      const double gd = !cubic ? RN_MUL(kp.g2[p], q[d]) : pair_grad_aniso_d(kp.g2[p], kp.delta[p], q, d);
       jf[a] = RN_FMA(-gd, s[b], jf[a]);
       jf[b] = RN_FMA(gd, s[a], jf[b]);
     }
@@ -281,7 +285,7 @@ __device__ __forceinline__ double cdiff(double lo, double hi) { return RN_SUB(hi
 // face fluxes before its CTA barrier: phi_cell_rhs0 returns
 // r0_a = eps T da/dphi_a + (T/eps) domega/dphi_a + dpsi/dphi_a (O4.2-4.4,
 // 4.7-4.8), phi_cell_finish adds the divergence and does O4.9-4.11.
-template <int AN = -1>
+template <int AN = -1, int DM = -1>
 __device__ __forceinline__ void phi_cell_rhs0(const KParams &kp, const double *__restrict__ tab,
                                               const double ph[NPH], const double mu[NMU],
                                               const double gc[NPH][3], double r0[NPH]);
@@ -309,7 +313,7 @@ __device__ __forceinline__ void phi_cell_update(const KParams &kp, const double 
   phi_cell_update_div(kp, tab, ph, mu, gc, dsum, out);
 }
 
-template <int AN>
+template <int AN, int DM>
 __device__ __forceinline__ void phi_cell_rhs0(const KParams &kp, const double *__restrict__ tab,
                                               const double ph[NPH], const double mu[NMU],
                                               const double gc[NPH][3], double r0[NPH]) {
@@ -348,7 +352,7 @@ __device__ __forceinline__ void phi_cell_rhs0(const KParams &kp, const double *_
       for (int e = 0; e < 3; ++e) q[e] = ph[a] * gc[b][e] - ph[b] * gc[a][e];
       // raw centre differences (2 dx grad): q is 2 dx too large, g (degree 1)
       // as well, dad by (2 dx)^2 — g2c carries the 1/(2 dx)^2
-      if ((kp.dmask >> p) & 1) {
+      if (DM < 0 ? ((kp.dmask >> p) & 1) != 0 : ((DM >> p) & 1) != 0) {
         pair_grad_aniso(kp.g2c[p], kp.delta[p], q, g);
       } else {
 #pragma unroll

@@ -42,7 +42,9 @@ struct __align__(128) PhiSmemT {
 
 constexpr uint32_t PHI_STAGE_BYTES = (NPH * RXS * RY + TAB) * 8;
 
-template <bool ANISO, int SC>   // SC: 0 no shortcut code, 1 the round-1 vote (run-time flag), 2 skip-faces shortcuts
+// SC: 0 no shortcut code, 1 the round-1 vote (run-time flag), 2 skip-faces shortcuts;
+// DM: the anisotropic kernel's cubic-pair mask at compile time (-1: kp.dmask)
+template <bool ANISO, int SC, int DM = -1>
 #ifndef PF_PHI_MINB
 #define PF_PHI_MINB (512 / NTHR)
 #endif
@@ -64,7 +66,7 @@ __global__ void __launch_bounds__(NTHR, ANISO ? PF_PHI_MINB : PF_PHI_MINB_ISO)
 // the face and cell routines specialised for this kernel's model: each of the
 // two kernels carries only its own code (measured: iso -1.8 %, aniso -6 %;
 // 35 % less code, fewer instruction-fetch stalls)
-#define PF_AN (ANISO ? 1 : 0)
+#define PF_AN (ANISO ? 1 : 0), DM
 
   auto slot = [&](int k) { return PNS == 4 ? (k - k0 + 1) & 3 : (k - k0 + 1) % PNS; };
   auto parity = [&](int k) { return (uint32_t)(((k - k0 + 1) / PNS) & 1); };
@@ -354,10 +356,16 @@ __global__ void __launch_bounds__(NTHR, ANISO ? PF_PHI_MINB : PF_PHI_MINB_ISO)
 // not inside a stream capture).
 static int g_phi_slots[2] = {1, 1};   // resident CTAs on the GPU, [ANISO]
 
+// the cubic pairs of the solid-liquid interfaces only (pairs (a, l): p = 2, 4, 5),
+// the model of C5 (delta_sl): compiled without the per-pair mask test
+constexpr int DM_SL = (1 << pair_of(0, LIQ)) | (1 << pair_of(1, LIQ)) | (1 << pair_of(2, LIQ));
+
 void prepare_phi_tiled() {
   const int sa = (int)sizeof(PhiSmemT<true>), si = (int)sizeof(PhiSmemT<false>);
   cudaFuncSetAttribute(phi_tiled_kernel<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sa);
   cudaFuncSetAttribute(phi_tiled_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sa);
+  cudaFuncSetAttribute(phi_tiled_kernel<true, 0, DM_SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, sa);
+  cudaFuncSetAttribute(phi_tiled_kernel<true, 2, DM_SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, sa);
   cudaFuncSetAttribute(phi_tiled_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, si);
   cudaFuncSetAttribute(phi_tiled_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, si);
   g_phi_slots[0] = grid_slots(phi_tiled_kernel<false, 1>, NTHR, si);
@@ -377,9 +385,13 @@ void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, con
   // run-time check compiled in (its code without it, or with the SC = 2 vote
   // in the same kernel, measured +1.7 %: the compiler's schedule, not the
   // check, decides there)
+  const bool sl = kp.dmask == DM_SL;
   if (kp.shortcuts) {
-    if (kp.aniso) phi_tiled_kernel<true, 2><<<grd, blk, sm, s>>>(tm, kp, b, kz);
+    if (kp.aniso && sl) phi_tiled_kernel<true, 2, DM_SL><<<grd, blk, sm, s>>>(tm, kp, b, kz);
+    else if (kp.aniso) phi_tiled_kernel<true, 2><<<grd, blk, sm, s>>>(tm, kp, b, kz);
     else phi_tiled_kernel<false, 2><<<grd, blk, sm, s>>>(tm, kp, b, kz);
+  } else if (kp.aniso && sl) {
+    phi_tiled_kernel<true, 0, DM_SL><<<grd, blk, sm, s>>>(tm, kp, b, kz);
   } else if (kp.aniso) {
     phi_tiled_kernel<true, 0><<<grd, blk, sm, s>>>(tm, kp, b, kz);
   } else {
