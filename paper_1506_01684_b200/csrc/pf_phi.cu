@@ -365,7 +365,6 @@ void prepare_phi_tiled() {
   cudaFuncSetAttribute(phi_tiled_kernel<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sa);
   cudaFuncSetAttribute(phi_tiled_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sa);
   cudaFuncSetAttribute(phi_tiled_kernel<true, 0, DM_SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, sa);
-  cudaFuncSetAttribute(phi_tiled_kernel<true, 2, DM_SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, sa);
   cudaFuncSetAttribute(phi_tiled_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, si);
   cudaFuncSetAttribute(phi_tiled_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, si);
   g_phi_slots[0] = grid_slots(phi_tiled_kernel<false, 1>, NTHR, si);
@@ -385,10 +384,13 @@ void launch_phi_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, con
   // run-time check compiled in (its code without it, or with the SC = 2 vote
   // in the same kernel, measured +1.7 %: the compiler's schedule, not the
   // check, decides there)
+  // the solid-liquid anisotropic kernel runs without the vote even with
+  // shortcuts on: its skip-faces variant measured slower in every scenario
+  // (256^3 interface / solid / liquid: 0.89 / 0.92 / 0.85 vs 0.80 / 0.81 / 0.79
+  // ms, profiles/r02_scenarios_aniso.md) — bitwise the same results either way
   const bool sl = kp.dmask == DM_SL;
-  if (kp.shortcuts) {
-    if (kp.aniso && sl) phi_tiled_kernel<true, 2, DM_SL><<<grd, blk, sm, s>>>(tm, kp, b, kz);
-    else if (kp.aniso) phi_tiled_kernel<true, 2><<<grd, blk, sm, s>>>(tm, kp, b, kz);
+  if (kp.shortcuts && !(kp.aniso && sl)) {
+    if (kp.aniso) phi_tiled_kernel<true, 2><<<grd, blk, sm, s>>>(tm, kp, b, kz);
     else phi_tiled_kernel<false, 2><<<grd, blk, sm, s>>>(tm, kp, b, kz);
   } else if (kp.aniso && sl) {
     phi_tiled_kernel<true, 0, DM_SL><<<grd, blk, sm, s>>>(tm, kp, b, kz);

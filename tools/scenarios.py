@@ -1,7 +1,8 @@
 """Scenario benchmarks: per-sweep time on
 blocks that are all interface (C4 front), all solid (Voronoi grains with grain
 boundaries, no liquid) or all liquid, with and without region shortcuts
-(NEXT-1).  Prints a markdown table; 256^3 blocks by default (N env)."""
+(NEXT-1).  Prints a markdown table; 256^3 blocks by default (N env); ANISO=1: the
+C5 model (cubic anisotropy on the solid-liquid pairs)."""
 import os
 import sys
 
@@ -13,7 +14,8 @@ from paper_1506_01684_b200 import pf
 
 n = int(os.environ.get("N", 256))
 pd = gen.load_params("v1")
-cfg = gen.load_config("c4")
+aniso = os.environ.get("ANISO") == "1"
+cfg = gen.load_config("c5" if aniso else "c4")
 spec = gen.spec_from_config(cfg, n, n)
 scen = {}
 spec.layer_height = n / 2
