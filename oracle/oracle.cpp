@@ -208,7 +208,10 @@ template <class R> inline R pair_energy(const or_params &p, int a, int b, const 
 /* Components d in [d0, d1) of g_ab(q) (the face fluxes need only the normal
  * component d, the centre term all three). */
 template <class R> inline void pair_grad_range(const or_params &p, int a, int b, const R q_[3], R gq[3], int d0, int d1) {
-  if (!p.aniso) {  /* e = gamma |q|^2  ->  g = 2 gamma q */
+  /* e = gamma |q|^2  ->  g = 2 gamma q; also for a pair without anisotropy
+     (delta_ab = 0: a_c = 1 identically, reading R3), so a model with cubic
+     anisotropy on some pairs only is counted with the others isotropic */
+  if (!p.aniso || p.delta[a][b] == 0.0) {
     for (int d = d0; d < d1; ++d) gq[d] = R(2.0 * p.gamma[a][b]) * q_[d];
     return;
   }
