@@ -40,6 +40,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
         return LIB
     src = csrc or CSRC
     inc, libdir = _nccl_dirs()
+    os.makedirs(os.path.dirname(os.path.abspath(out or LIB)), exist_ok=True)   # build/ is not in git
     cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
            "-I", inc, "-I", os.path.join(os.path.dirname(HERE), "include"),
