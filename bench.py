@@ -34,6 +34,7 @@ CONFIG = "c4"
 # Algorithmic work per LUP: FLOPs counted from the oracle
 # (oracle.count_flops, isotropic), compulsory FP64 bytes.
 BYTES_PHI, BYTES_MU = 80, 96
+BYTES_FUSED = 128   # fused mu(n) + phi(n+1): read phi^n, phi^{n+1}, mu^n; write mu^{n+1}, phi^{n+2}
 PEAK_FP64_DERIVED = 148 * 64 * 2 * 1.965e9 / 1e12   # TFLOP/s: SMs x FP64 FMA/clk x 2 x max clock
 # SURVEY.md §8(d)'s counted FLOP/LUP (a scratch op count of O4/O5 made during
 # the survey), reported beside the oracle's own count
@@ -320,6 +321,39 @@ def run_gpu(args):
                       "off for the exact FLOP count"}
         ctx.set_shortcuts(False)
         ctx.set_timing(False)
+    # the same windows' length with fused steps (pf_set_fusion: the mu-sweep of
+    # step n and the phi-sweep of step n+1 as one kernel, 128 B/LUP instead of
+    # 176; bitwise the same results), beside the headline, which keeps the two
+    # sweeps so that each has its own roofline line
+    fu = None
+    if not args.graph and not args.no_fused:
+        try:
+            ctx.set_fusion(True)
+        except RuntimeError as ex:   # no room for the third phi copy
+            fu = {"value": None, "what": f"not run: {ex}"}
+        if fu is None:
+            ctx.set_timing(True)
+            barrier()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            ctx.step(args.steps)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            inf = ctx.info()
+            fu_ms = max_over_ranks(e0.elapsed_time(e1))
+            fk = inf.ms_fused / max(1, inf.fused_launches)
+            fu = {"value": round(cells_local * world * args.steps / (fu_ms / 1e3) / 1e6, 2),
+                  "ms_per_step": round(fu_ms / args.steps, 4), "fused_ms": round(fk, 4),
+                  "fused_launches": int(inf.fused_launches),
+                  "phi_ms": round(inf.ms_phi / max(1, inf.phi_launches), 4),
+                  "mu_ms": round(inf.ms_mu / max(1, inf.mu_launches), 4),
+                  "fused_bytes_per_lup": BYTES_FUSED,
+                  "fused_gbs": round(BYTES_FUSED * cells_local / (fk / 1e3) / 1e9, 1),
+                  "what": "fused steps on (pf_set_fusion): pf_step(steps) = phi-sweep, steps-1 fused mu(n)+phi(n+1) "
+                          "kernels, mu-sweep; bitwise-identical results; the headline keeps the separate sweeps"}
+            ctx.set_fusion(False)
+        ctx.set_timing(False)
     if args.graph:
         ctx.set_timing(True)
         ctx.step(min(args.steps, 10))
@@ -466,6 +500,7 @@ def run_gpu(args):
                     "job": {"value": round(e2e_job, 2) if e2e_job else None, "steps": args.steps,
                             "what": "pf_write(pinned host state) once + pf_step(steps) + pf_read(pinned host) once"}},
             "shortcuts": sc,
+            "fused": fu,
             "gpu_launches": launches,
             "clocks": clk,
         }
@@ -522,6 +557,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3, help="timed windows of --steps steps each; the median is reported")
     ap.add_argument("--no-interface", action="store_true", help="skip the all-guards-open sweep measurement")
     ap.add_argument("--no-shortcuts", action="store_true", help="skip the region-shortcut window")
+    ap.add_argument("--no-fused", action="store_true", help="skip the fused-step window")
     ap.add_argument("--graph", action="store_true", help="replay each step as a CUDA graph (single rank)")
     ap.add_argument("--grid", type=int, nargs=3, metavar=("NX", "NY", "NZ"),
                     help="global grid overriding the config's (its physics and init recipe kept)")

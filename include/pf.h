@@ -142,6 +142,10 @@ typedef struct {
                                  family (CUDA events on the launching stream)      */
   int64_t launches;           /* kernels launched by pf_step so far                */
   int64_t phi_launches, mu_launches; /* sweep launches counted in ms_phi / ms_mu   */
+  double ms_fused;            /* accumulated device time of the fused kernel       */
+  int64_t fused_launches;     /* fused launches counted in ms_fused                */
+  int32_t fusion;             /* 1 if pf_set_fusion is on                          */
+  int32_t pad_;
 } pf_info_t;
 
 typedef struct pf_ctx pf_ctx;
@@ -277,6 +281,26 @@ pf_status pf_set_timing(pf_ctx *c, int32_t on);
  * configuration whose FLOP count per cell is exact.
  * Errors: PF_ERR_ARG (NULL), PF_ERR_STATE after an error. */
 pf_status pf_set_shortcuts(pf_ctx *c, int32_t on);
+
+/* Fused steps on (1) or off (0) for the following pf_step calls.  On: within
+ * one pf_step(n), n >= 2, the mu-sweep of step k and the phi-sweep of step k+1
+ * (Algorithm 1 lines 4 and 1 of consecutive iterations) run
+ * as ONE kernel: the phi-sweep reads mu at the cell centre only (D3C1,
+ * PAPER.md:176-177), which that kernel has just computed, and both read the
+ * same phi^{k+1} tiles — 128 B of HBM traffic per cell and step instead of
+ * 176.  Every state the caller (or the moving-window check, the NaN watchdog)
+ * sees is a complete time level, and results are bitwise those of fusion off
+ * (tests/test_gpu_fused.py).  Applies to the tiled sweeps with overlap 0 / 1
+ * region shortcuts off and graph = 0; otherwise pf_step runs the separate
+ * sweeps.  Default off, like the region shortcuts (an opt-in speed setting
+ * with bitwise the same results): measured at 512^3 the
+ * isotropic step is 3 % faster fused, the anisotropic one 19 % slower (its
+ * fused kernel is register-bound).
+ * The first call with on = 1 allocates a third phi copy (4 doubles per cell
+ * of the block, ghosts and window slack included).
+ * Errors: PF_ERR_ARG (NULL), PF_ERR_STATE after an error, PF_ERR_CUDA if that
+ * copy does not fit (fusion stays off; the context stays usable). */
+pf_status pf_set_fusion(pf_ctx *c, int32_t on);
 
 pf_status pf_info(pf_ctx *c, pf_info_t *out);
 

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpf.so")
-SOURCES = ["pf_runtime.cu", "pf_kernels.cu", "pf_phi.cu", "pf_mu.cu", "pf_mesh.cu"]
+SOURCES = ["pf_runtime.cu", "pf_kernels.cu", "pf_phi.cu", "pf_mu.cu", "pf_fused.cu", "pf_mesh.cu"]
 HEADERS = ["pf_dev.cuh", "pf_kernels.cuh", "pf_tile.cuh"]
 
 

@@ -26,6 +26,14 @@ constexpr int XO = 4;  // column of interior i = 0 within a padded row (i = -1 a
 #ifndef PF_MU_TY
 #define PF_MU_TY 8
 #endif
+// the fused mu(n) + phi(n+1) kernel (pf_fused.cu): 16 x 8 at 3 CTAs / SM
+#ifndef PF_FUSED_TX
+#define PF_FUSED_TX 16
+#endif
+#ifndef PF_FUSED_TY
+#define PF_FUSED_TY 8
+#endif
+constexpr int FUSED_TILE_X = PF_FUSED_TX, FUSED_TILE_Y = PF_FUSED_TY;
 constexpr int PHI_TILE_X = PF_PHI_TX, PHI_TILE_Y = PF_PHI_TY, MU_TILE_X = PF_MU_TX, MU_TILE_Y = PF_MU_TY;
 
 // TMA descriptors of one block's fields in one time level (encoded on the host
@@ -103,6 +111,16 @@ void launch_mu_tiled(cudaStream_t s, const KParams &kp, const BlockView &b, cons
 // z-slab view): bitwise the cells' values of the whole-block launch
 void launch_mu_tiles(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm, int tx0, int tx1,
                      int ty0, int ty1);
+// the fused kernel (pf_fused.cu): b is the mu-sweep view of step n (phi =
+// phi^n, phin = phi^{n+1}, mu = mu^n, out = mu^{n+1}, tab = step n's rows),
+// tm its maps with the fused tile box; fo the phi^{n+2} output and step n+1's
+// table rows.  Bitwise the mu-sweep of step n followed by the phi-sweep of n+1.
+struct FusedOut {
+  double *phi2[NPH];      // phi^{n+2}, offset like BlockView::out
+  const double *tabp;     // table row of local plane 0 at step n+1
+};
+void prepare_fused();
+void launch_fused(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm, const FusedOut &fo);
 int mu_tiles_x(int nx);   // CTA tiles of the mu-sweep along x / y
 int mu_tiles_y(int ny);
 void launch_copy(cudaStream_t s, const CopyOp *d_ops, int nops, int64_t nctas);

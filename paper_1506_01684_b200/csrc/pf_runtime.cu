@@ -38,12 +38,15 @@ struct Block {
   int nx, ny, nz;
   int64_t x0, y0, z0;        // global offset of the interior
   int64_t pitch, plane, nplanes_alloc;
-  double *phi[2][NPH];       // two copies (src/dst), allocation bases
+  double *phi[3][NPH];       // two copies (src/dst), allocation bases; a third for the
+                             // fused kernel's phi^{n+2} (pf_set_fusion), rotated with them
   double *mu[2][NMU];
   int woff;                  // window offset (planes)
-  CUtensorMap tphi[2][NPH];  // TMA maps per time level: phi tile box (phi-sweep tile),
-  CUtensorMap tphim[2][NPH]; //   phi tile box (mu-sweep tile),
+  CUtensorMap tphi[3][NPH];  // TMA maps per time level: phi tile box (phi-sweep tile),
+  CUtensorMap tphim[3][NPH]; //   phi tile box (mu-sweep tile),
   CUtensorMap tmu[2][NMU];   //   mu tile box (mu-sweep tile)
+  CUtensorMap tphif[3][NPH]; //   phi / mu tile boxes of the fused kernel
+  CUtensorMap tmuf[2][NMU];
 };
 
 struct Plan {                // halo plan of one field in one copy
@@ -80,7 +83,11 @@ struct pf_ctx {
   ncclComm_t comm_mu = nullptr;
   double *d_tab = nullptr;
   int64_t tab_planes = 0;
-  Plan plan[2][2];                 // [field 0=phi 1=mu][copy]
+  Plan plan[2][3];                 // [field 0=phi 1=mu][copy] (copy 2: phi only, with fusion)
+  // fused mu(n) + phi(n+1) steps (pf_set_fusion): a third phi copy, the table
+  // rows of the next step
+  bool fusion = false, phi3 = false;
+  double *d_tab2 = nullptr;
   std::vector<Peer> peers[2];      // per field
   double *d_send[2] = {nullptr, nullptr}, *d_recv[2] = {nullptr, nullptr};
   int64_t send_total[2] = {0, 0}, recv_total[2] = {0, 0};
@@ -100,8 +107,8 @@ struct pf_ctx {
   size_t ev_used = 0;
   struct Span { int kind; size_t e0, e1; int nlaunch; };
   std::vector<Span> spans;
-  double ms[4] = {0, 0, 0, 0};
-  int64_t launches = 0, phi_launches = 0, mu_launches = 0;
+  double ms[5] = {0, 0, 0, 0, 0};  // phi, mu, halo, other, fused
+  int64_t launches = 0, phi_launches = 0, mu_launches = 0, fused_launches = 0;
   // box of this rank
   int64_t box_nx = 0, box_ny = 0, box_nz = 0, box_x0 = 0, box_y0 = 0, box_z0 = 0;
   // marching cubes (pf_mesh): block pointer table, scan scratch, host-output staging
@@ -121,6 +128,7 @@ struct pf_ctx {
   struct SlabIO {
     int H = 0, S = 0;                      // slab height, slab count
     int woff = 0;                          // window offset the copy lists were built for
+    const double *phi0[2] = {nullptr, nullptr};   // and the phi copies' addresses
     std::vector<CopyOp *> ops[2][2];       // [field][copy][slab]
     std::vector<int> nops[2][2];
     std::vector<int64_t> nctas[2][2];
@@ -279,14 +287,23 @@ pf_status encode_map(pf_ctx *c, CUtensorMap *m, double *base, const Block &b, in
 }
 
 pf_status encode_maps(pf_ctx *c, Block &b) {
-  for (int cp = 0; cp < 2; ++cp) {
+  for (int cp = 0; cp < 3; ++cp) {
+    if (!b.phi[cp][0]) continue;
+    for (int a = 0; a < NPH; ++a)
+      CKS(encode_map(c, &b.tphif[cp][a], b.phi[cp][a], b, FUSED_TILE_X + 4, FUSED_TILE_Y + 2));
+    if (cp < 2)
+      for (int q = 0; q < NMU; ++q)
+        CKS(encode_map(c, &b.tmuf[cp][q], b.mu[cp][q], b, FUSED_TILE_X + 4, FUSED_TILE_Y + 2));
+  }
+  for (int cp = 0; cp < 3; ++cp) {
+    if (!b.phi[cp][0]) continue;
     // tile boxes start one column left of the ring (16-byte aligned x): tile width + 4;
     // phi-sweep tiles are PHI_TILE_Y high, mu-sweep tiles MU_TILE_Y
     for (int a = 0; a < NPH; ++a) {
       CKS(encode_map(c, &b.tphi[cp][a], b.phi[cp][a], b, PHI_TILE_X + 4, PHI_TILE_Y + 2));
       CKS(encode_map(c, &b.tphim[cp][a], b.phi[cp][a], b, MU_TILE_X + 4, MU_TILE_Y + 2));
     }
-    for (int q = 0; q < NMU; ++q) {
+    for (int q = 0; q < NMU && cp < 2; ++q) {
       CKS(encode_map(c, &b.tmu[cp][q], b.mu[cp][q], b, MU_TILE_X + 4, MU_TILE_Y + 2));
     }
   }
@@ -303,6 +320,15 @@ TmaMaps maps_of(const pf_ctx *c, const Block &b, int field) {
     t.phin[a] = b.tphim[d][a];
   }
   for (int q = 0; q < NMU; ++q) t.mu[q] = b.tmu[s][q];
+  return t;
+}
+
+// maps of the fused kernel at the current state: phi^n, phi^{n+1}, mu^n
+TmaMaps maps_fused(const pf_ctx *c, const Block &b) {
+  TmaMaps t;
+  const int s = c->cur, d = c->cur ^ 1;
+  for (int a = 0; a < NPH; ++a) { t.phi[a] = b.tphif[s][a]; t.phin[a] = b.tphif[d][a]; }
+  for (int q = 0; q < NMU; ++q) t.mu[q] = b.tmuf[s][q];
   return t;
 }
 
@@ -360,7 +386,7 @@ pf_status build_plans(pf_ctx *c) {
     if (c->send_total[field]) CK(cudaMalloc(&c->d_send[field], c->send_total[field] * sizeof(double)));
     if (c->recv_total[field]) CK(cudaMalloc(&c->d_recv[field], c->recv_total[field] * sizeof(double)));
 
-    for (int copy = 0; copy < 2; ++copy) {
+    for (int copy = 0; copy < (field == 0 && c->phi3 ? 3 : 2); ++copy) {
       std::vector<CopyOp> local, pack, unpack;
       Plan &pl = c->plan[field][copy];
       // local copies: both ends on this rank
@@ -508,6 +534,7 @@ pf_status collect_timing(pf_ctx *c) {
     c->ms[s.kind] += ms;
     if (s.kind == 0) c->phi_launches += s.nlaunch;
     if (s.kind == 1) c->mu_launches += s.nlaunch;
+    if (s.kind == 4) c->fused_launches += s.nlaunch;
   }
   c->spans.clear();
   c->ev_used = 0;
@@ -653,9 +680,12 @@ void slab_free(pf_ctx *c);
 
 pf_status slab_setup(pf_ctx *c) {
   auto &io = c->sio;
-  if (io.S && io.woff == c->blocks[0].woff) return PF_OK;
+  const Block &b0 = c->blocks[0];
+  if (io.S && io.woff == b0.woff && io.phi0[0] == b0.phi[0][0] && io.phi0[1] == b0.phi[1][0]) return PF_OK;
   if (io.S) slab_free(c);   // the window moved since: the copy lists hold plane addresses
-  io.woff = c->blocks[0].woff;
+  io.woff = b0.woff;
+  io.phi0[0] = b0.phi[0][0];   // the copy lists hold field addresses: fusion rotates the phi copies
+  io.phi0[1] = b0.phi[1][0];
   const int nz = c->blocks[0].nz;
 #ifndef PF_SLABS
 #define PF_SLABS 32   // measured at 512^3: 16 -> 146.1, 32 -> 144.4, 64 -> 146.1 ms per step
@@ -1152,6 +1182,7 @@ pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
   if (build_plans(c) != PF_OK) return bail(c->status);
   prepare_phi_tiled();
   prepare_mu_tiled();
+  prepare_fused();
   if (cudaDeviceSynchronize() != cudaSuccess) { fail(c, PF_ERR_CUDA, "setup sync"); return bail(PF_ERR_CUDA); }
   *out = c;
   return PF_OK;
@@ -1361,6 +1392,95 @@ pf_status enqueue_step(pf_ctx *c, bool graph) {
   return PF_OK;
 }
 
+// ---- fused steps (pf_set_fusion): the mu-sweep of step n and the phi-sweep
+// of step n+1 in one kernel (pf_fused.cu).  A run of steps becomes
+//   phi-half(n0), fused(n0) .. fused(n1-2), mu-half(n1-1)
+// and every state a caller, the window check or the NaN watchdog sees is a
+// complete time level (the run is cut there).  Bitwise the plain sequence.
+bool fusable(const pf_ctx *c) {
+  return c->fusion && c->phi3 && c->p.variant != 1 && (c->p.overlap == 0 || c->p.overlap == 1) && !c->kp.shortcuts &&
+         !c->p.graph;
+}
+
+// swap phi copy `a` with the third copy: addresses, TMA maps, the phi halo plan
+void rotate_phi(pf_ctx *c, int a) {
+  for (auto &b : c->blocks)
+    for (int q = 0; q < NPH; ++q) {
+      std::swap(b.phi[a][q], b.phi[2][q]);
+      std::swap(b.tphi[a][q], b.tphi[2][q]);
+      std::swap(b.tphim[a][q], b.tphim[2][q]);
+      std::swap(b.tphif[a][q], b.tphif[2][q]);
+    }
+  std::swap(c->plan[0][a], c->plan[0][2]);
+  invalidate_graphs(c);   // captured launches hold addresses
+}
+
+// Algorithm 1 lines 1-3: table rows of step n, phi-sweep, phi^{n+1} ghosts
+pf_status enqueue_phi_half(pf_ctx *c) {
+  {
+    TimedSpan ts(c, 3, 0);
+    launch_table(c->stream, c->d_tab, c->tab_planes, c->tp, c->step, c->zorig, nullptr);
+    c->launches++;
+  }
+  {
+    TimedSpan ts(c, 0, (int)c->blocks.size());
+    for (const auto &b : c->blocks) {
+      launch_phi_tiled(c->stream, c->kp, view(c, b, 0), maps_of(c, b, 0));
+      c->launches++;
+    }
+  }
+  CK(cudaGetLastError());
+  return exchange(c, 0, c->cur ^ 1);
+}
+
+// lines 4-6: mu-sweep, mu^{n+1} ghosts (mode 0: beside what follows)
+pf_status enqueue_mu_half(pf_ctx *c) {
+  CKS(join_mu(c));
+  {
+    TimedSpan ts(c, 1, (int)c->blocks.size());
+    for (const auto &b : c->blocks) {
+      launch_mu_tiled(c->stream, c->kp, view(c, b, 1), maps_of(c, b, 1), MU_FULL);
+      c->launches++;
+    }
+  }
+  CK(cudaGetLastError());
+  if (c->p.overlap != 0) return exchange(c, 1, c->cur ^ 1);
+  CK(cudaEventRecord(c->ev_mu_done, c->stream));
+  CK(cudaStreamWaitEvent(c->cstream, c->ev_mu_done, 0));
+  CKS(exchange(c, 1, c->cur ^ 1, true));
+  CK(cudaEventRecord(c->ev_mu_halo, c->cstream));
+  c->mu_pending = true;
+  return PF_OK;
+}
+
+// lines 4-6 of step n and 1-3 of step n+1: one fused kernel per block, then the
+// mu^{n+1} and phi^{n+2} ghosts (the next fused kernel reads both stencils)
+pf_status enqueue_fused(pf_ctx *c) {
+  CKS(join_mu(c));
+  {
+    TimedSpan ts(c, 3, 0);
+    launch_table(c->stream, c->d_tab2, c->tab_planes, c->tp, c->step + 1, c->zorig, nullptr);
+    c->launches++;
+  }
+  {
+    TimedSpan ts(c, 4, (int)c->blocks.size());
+    for (const auto &b : c->blocks) {
+      FusedOut fo;
+      const int64_t o = cell_off(b, 0, 0, 0);
+      for (int a = 0; a < NPH; ++a) fo.phi2[a] = b.phi[2][a] + o;
+      fo.tabp = c->d_tab2 + (b.z0 + 1) * TAB;
+      launch_fused(c->stream, c->kp, view(c, b, 1), maps_fused(c, b), fo);
+      c->launches++;
+    }
+  }
+  CK(cudaGetLastError());
+  const int c0 = c->cur;
+  rotate_phi(c, c0);                // phi^{n+2} takes the place of the dead phi^n
+  std::swap(c->d_tab, c->d_tab2);   // step n+1's rows become the current ones
+  CKS(exchange(c, 1, c0 ^ 1));
+  return exchange(c, 0, c0);
+}
+
 // Capture one step from src copy c->cur into c->gexec[c->cur].
 pf_status capture_step(pf_ctx *c) {
   cudaGraph_t g = nullptr;
@@ -1393,6 +1513,30 @@ pf_status pf_step(pf_ctx *c, int64_t n) {
   }
   // CUDA graphs (pf_params.graph = 1) for single-rank runs without per-sweep
   // timing: one launch per step instead of five-plus — same results, bit for bit
+  if (fusable(c) && n >= 2) {
+    bool ahead = false;   // phi^{n+1} of the current step computed (and its ghosts)
+    for (int64_t s = 0; s < n; ++s) {
+      const int64_t nx1 = c->step + 1;
+      const bool nan_due = c->p.nan_check_every > 0 && nx1 % c->p.nan_check_every == 0;
+      const bool end = s == n - 1 || nan_due || (c->p.window && nx1 >= c->next_check);
+      if (!ahead) CKS(enqueue_phi_half(c));
+      if (end) CKS(enqueue_mu_half(c));
+      else CKS(enqueue_fused(c));
+      ahead = !end;
+      c->cur ^= 1;
+      c->step += 1;
+      if (end) {
+        if ((c->p.window && c->step >= c->next_check) || nan_due) CKS(join_mu(c));
+        CKS(window_check(c));
+        if (nan_due) CKS(nan_check(c));
+      }
+      if (c->timing && c->spans.size() > 4096) CKS(collect_timing(c));
+    }
+    CKS(join_mu(c));
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaGetLastError());
+    return collect_timing(c);
+  }
   const bool use_graph = !c->timing && c->g.nranks == 1 && c->p.graph && n > 0;
   if (use_graph) {
     CKS(join_mu(c));
@@ -1626,7 +1770,37 @@ pf_status pf_set_timing(pf_ctx *c, int32_t on) {
   CKS(collect_timing(c));
   c->timing = on != 0;
   for (double &m : c->ms) m = 0;
-  c->phi_launches = c->mu_launches = 0;
+  c->phi_launches = c->mu_launches = c->fused_launches = 0;
+  return PF_OK;
+}
+
+pf_status pf_set_fusion(pf_ctx *c, int32_t on) {
+  CKS(check_state(c, false));
+  if (on && !c->phi3) {
+    // the third phi copy (and the second table): allocated once, on first use
+    CKS(join_mu(c));
+    CK(cudaStreamSynchronize(c->stream));
+    bool ok = cudaMalloc(&c->d_tab2, (size_t)c->tab_planes * TAB * sizeof(double)) == cudaSuccess;
+    for (auto &b : c->blocks) {
+      const size_t bytes = (size_t)b.plane * b.nplanes_alloc * sizeof(double);
+      for (int a = 0; a < NPH && ok; ++a) {
+        ok = cudaMalloc(&b.phi[2][a], bytes) == cudaSuccess;
+        if (ok) ok = cudaMemset(b.phi[2][a], 0, bytes) == cudaSuccess;
+      }
+    }
+    if (!ok) {   // not enough device memory: fusion stays off, the context stays usable
+      cudaGetLastError();
+      for (auto &b : c->blocks)
+        for (int a = 0; a < NPH; ++a) if (b.phi[2][a]) { cudaFree(b.phi[2][a]); b.phi[2][a] = nullptr; }
+      if (c->d_tab2) { cudaFree(c->d_tab2); c->d_tab2 = nullptr; }
+      c->err = "pf_set_fusion: no device memory for the third phi copy";
+      return PF_ERR_CUDA;
+    }
+    c->phi3 = true;
+    for (auto &b : c->blocks) CKS(encode_maps(c, b));
+    CKS(build_plans(c));
+  }
+  c->fusion = on != 0;
   return PF_OK;
 }
 
@@ -1648,6 +1822,7 @@ pf_status pf_info(pf_ctx *c, pf_info_t *o) {
   o->timing = c->timing;
   o->ms_phi = c->ms[0]; o->ms_mu = c->ms[1]; o->ms_halo = c->ms[2]; o->ms_other = c->ms[3];
   o->launches = c->launches; o->phi_launches = c->phi_launches; o->mu_launches = c->mu_launches;
+  o->ms_fused = c->ms[4]; o->fused_launches = c->fused_launches; o->fusion = c->fusion ? 1 : 0;
   return c->status == PF_OK ? PF_OK : PF_ERR_STATE;
 }
 
@@ -1720,13 +1895,13 @@ void pf_destroy(pf_ctx *c) {
   cudaSetDevice(c->g.device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto &b : c->blocks) {
-    for (int cp = 0; cp < 2; ++cp) {
+    for (int cp = 0; cp < 3; ++cp) {
       for (int a = 0; a < NPH; ++a) if (b.phi[cp][a]) cudaFree(b.phi[cp][a]);
-      for (int q = 0; q < NMU; ++q) if (b.mu[cp][q]) cudaFree(b.mu[cp][q]);
+      for (int q = 0; q < NMU && cp < 2; ++q) if (b.mu[cp][q]) cudaFree(b.mu[cp][q]);
     }
   }
   for (int f = 0; f < 2; ++f) {
-    for (int cp = 0; cp < 2; ++cp) {
+    for (int cp = 0; cp < 3; ++cp) {
       if (c->plan[f][cp].d_local) cudaFree(c->plan[f][cp].d_local);
       if (c->plan[f][cp].d_unpack) cudaFree(c->plan[f][cp].d_unpack);
     }
@@ -1735,6 +1910,7 @@ void pf_destroy(pf_ctx *c) {
   }
   slab_free(c);
   if (c->d_tab) cudaFree(c->d_tab);
+  if (c->d_tab2) cudaFree(c->d_tab2);
   if (c->d_red) cudaFree(c->d_red);
   if (c->d_step) cudaFree(c->d_step);
   invalidate_graphs(c);

@@ -28,7 +28,7 @@ PF_OK, PF_ERR_CONFIG, PF_ERR_NUMERICAL, PF_ERR_CUDA, PF_ERR_COMM, PF_ERR_STATE, 
 STATUS_NAMES = {0: "PF_OK", -1: "PF_ERR_CONFIG", -2: "PF_ERR_NUMERICAL", -3: "PF_ERR_CUDA", -4: "PF_ERR_COMM",
                 -5: "PF_ERR_STATE", -6: "PF_ERR_ARG", -7: "PF_ERR_IO"}
 EXPORTS = ["pf_nccl_unique_id", "pf_halo_plan", "pf_create", "pf_init", "pf_write", "pf_set_time", "pf_step", "pf_read",
-           "pf_step_io", "pf_save", "pf_load", "pf_mesh", "pf_mesh_table", "pf_set_timing", "pf_set_shortcuts", "pf_info", "pf_last_error",
+           "pf_step_io", "pf_save", "pf_load", "pf_mesh", "pf_mesh_table", "pf_set_timing", "pf_set_shortcuts", "pf_set_fusion", "pf_info", "pf_last_error",
            "pf_destroy"]
 
 
@@ -63,7 +63,8 @@ class PfInfo(ctypes.Structure):
     _fields_ = [("nx_l", I64), ("ny_l", I64), ("nz_l", I64), ("x0", I64), ("y0", I64), ("z0", I64),
                 ("step", I64), ("z_origin", I64), ("shifts", I64), ("last_front", I64),
                 ("nblocks_local", I32), ("timing", I32), ("ms_phi", D), ("ms_mu", D), ("ms_halo", D),
-                ("ms_other", D), ("launches", I64), ("phi_launches", I64), ("mu_launches", I64)]
+                ("ms_other", D), ("launches", I64), ("phi_launches", I64), ("mu_launches", I64),
+                ("ms_fused", D), ("fused_launches", I64), ("fusion", I32), ("pad_", I32)]
 
 
 _lib = None
@@ -99,6 +100,7 @@ def lib():
         L.pf_mesh_table.argtypes = [vp]
         L.pf_set_timing.argtypes = [vp, I32]
         L.pf_set_shortcuts.argtypes = [vp, I32]
+        L.pf_set_fusion.argtypes = [vp, I32]
         L.pf_info.argtypes = [vp, ctypes.POINTER(PfInfo)]
         L.pf_last_error.argtypes = [vp]
         L.pf_last_error.restype = ctypes.c_char_p
@@ -279,6 +281,10 @@ class Context:
 
     def set_timing(self, on: bool):
         self._check(lib().pf_set_timing(self._c, 1 if on else 0))
+
+    def set_fusion(self, on: bool):
+        """Fused mu(n) + phi(n+1) steps on / off for the following steps (pf_set_fusion; bitwise the same results)."""
+        self._check(lib().pf_set_fusion(self._c, 1 if on else 0))
 
     def set_shortcuts(self, on: bool):
         """Region shortcuts on / off for the following steps (pf_set_shortcuts; bitwise the same results)."""

@@ -90,4 +90,6 @@ def test_gpu_arm_line():
     assert e2e["h2d_bytes_per_step"] == 48 * 128 ** 3 and e2e["d2h_bytes_per_step"] == 48 * 128 ** 3
     assert 0 < e2e["value"] < line["value"]
     assert line["gpu_launches"] >= 4 * line["steps"]
+    fu = line["fused"]
+    assert fu["value"] > 0 and fu["fused_launches"] == line["steps"] - 1 and fu["fused_ms"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(line["clocks"])
