@@ -291,8 +291,8 @@ pf_status pf_set_shortcuts(pf_ctx *c, int32_t on);
  * 176.  Every state the caller (or the moving-window check, the NaN watchdog)
  * sees is a complete time level, and results are bitwise those of fusion off
  * (tests/test_gpu_fused.py).  Applies to the tiled sweeps with overlap 0 / 1
- * region shortcuts off and graph = 0; otherwise pf_step runs the separate
- * sweeps.  Default off, like the region shortcuts (an opt-in speed setting
+ * and graph = 0, region shortcuts on or off; otherwise pf_step runs the
+ * separate sweeps.  Default off, like the region shortcuts (an opt-in speed setting
  * with bitwise the same results): measured at 512^3 the
  * isotropic step is 3 % faster fused, the anisotropic one 19 % slower (its
  * fused kernel is register-bound).

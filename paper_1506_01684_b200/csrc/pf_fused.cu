@@ -105,7 +105,8 @@ constexpr int kFusedUnroll = PF_FUSED_UNROLL;
 #define PF_FUSED_MINB (384 / NTHR)
 #endif
 
-template <bool ANISO, int DM>
+// SC: 0 no region-shortcut code, 2 the skip-faces vote of pf_phi.cu
+template <bool ANISO, int DM, int SC>
 __global__ void __launch_bounds__(NTHR, PF_FUSED_MINB)
     fused_kernel(const __grid_constant__ TmaMaps tm, KParams kp, BlockView b, FusedOut fo, int kz) {
   using Smem = FusedSmemT<ANISO>;
@@ -369,6 +370,31 @@ __global__ void __launch_bounds__(NTHR, PF_FUSED_MINB)
 
     // D (phi of step n+1): faces of plane k on phi^{n+1}; the own cell's centre
     // differences (read before E: slot(k-1) is refilled at A(k+1))
+    // region shortcut (SC = 2, pf_set_shortcuts; pf_phi.cu's vote on phi^{n+1}):
+    // a warp whose cells are simplex vertices with an identical D3C7 (D3C19)
+    // neighbourhood has exactly zero own faces and keeps phi^{n+2} = phi^{n+1}
+    bool skip = false;
+    if (SC == 2) {
+      if (__all_sync(0xffffffffu, is_vertex_bits(pn_c) || !active)) {
+        auto same = [](double x, double v) { return __double_as_longlong(x) == __double_as_longlong(v); };
+        bool mine = true;
+#pragma unroll
+        for (int a = 0; a < NPH; ++a) {
+          const double v = pn_c[a];
+          mine = mine && same(T(S.pn[sn][a], orow, oc - 1), v) && same(T(S.pn[sn][a], orow, oc + 1), v) &&
+                 same(T(S.pn[sn][a], orow - 1, oc), v) && same(T(S.pn[sn][a], orow + 1, oc), v) &&
+                 same(T(S.pn[sm][a], orow, oc), v) && same(T(S.pn[sp][a], orow, oc), v);
+          if (ANISO)
+            mine = mine && same(T(S.pn[sn][a], orow - 1, oc - 1), v) && same(T(S.pn[sn][a], orow - 1, oc + 1), v) &&
+                   same(T(S.pn[sn][a], orow + 1, oc - 1), v) && same(T(S.pn[sn][a], orow + 1, oc + 1), v) &&
+                   same(T(S.pn[sm][a], orow, oc - 1), v) && same(T(S.pn[sm][a], orow, oc + 1), v) &&
+                   same(T(S.pn[sm][a], orow - 1, oc), v) && same(T(S.pn[sm][a], orow + 1, oc), v) &&
+                   same(T(S.pn[sp][a], orow, oc - 1), v) && same(T(S.pn[sp][a], orow, oc + 1), v) &&
+                   same(T(S.pn[sp][a], orow - 1, oc), v) && same(T(S.pn[sp][a], orow + 1, oc), v);
+        }
+        skip = __all_sync(0xffffffffu, mine || !active) != 0;
+      }
+    }
     double gc[NPH][3], jzp[NPH], dpp[NPH];
     {
       double jf[NPH], lo[NPH], hi[NPH], gl[NPH][3], gh[NPH][3];
@@ -391,6 +417,17 @@ __global__ void __launch_bounds__(NTHR, PF_FUSED_MINB)
           }
         }
       };
+      if (SC == 2 && skip) {   // own faces exactly 0; the far faces as usual
+#pragma unroll
+        for (int a = 0; a < NPH; ++a) {
+          jzp[a] = 0.0;
+          dpp[a] = 0.0;
+          if (!ANISO) jzm[a] = 0.0;
+          S.pfx[a][ty][tx] = 0.0;
+          S.pfy[a][ty][tx] = 0.0;
+        }
+        far_faces();
+      } else {
       if (ANISO) tan_grad(sn, sm, sp, oc, orow, -1, gc);   // gown: the own cell's raw differences
       double pp[NPH];
 #pragma unroll
@@ -432,6 +469,7 @@ __global__ void __launch_bounds__(NTHR, PF_FUSED_MINB)
           gc[a][1] = T(S.pn[sn][a], orow + 1, oc) - T(S.pn[sn][a], orow - 1, oc);
           gc[a][2] = pp[a] - T(S.pn[sm][a], orow, oc);
         }
+      }
     }
     __syncthreads();  // E: the faces of plane k (both fields) complete
     // F: mu^{n+1}(i,j,k), then phi^{n+2}(i,j,k) with it
@@ -443,6 +481,10 @@ __global__ void __launch_bounds__(NTHR, PF_FUSED_MINB)
       mu_cell_update(kp, S.tab[sn], po_c, pn_c, mu_c, divf, mu1);
       b.out[0][o] = mu1[0];
       b.out[1][o] = mu1[1];
+      if (SC == 2 && skip) {
+#pragma unroll
+        for (int a = 0; a < NPH; ++a) fo.phi2[a][o] = pn_c[a];
+      } else {
       const double *tp = S.tabp[sn];
       double r0[NPH], q[NPH];
       phi_cell_rhs0<PF_AN>(kp, tp, pn_c, mu1, gc, r0);
@@ -463,6 +505,7 @@ __global__ void __launch_bounds__(NTHR, PF_FUSED_MINB)
       phi_cell_project(kp, pn_c, rhs, out);
 #pragma unroll
       for (int a = 0; a < NPH; ++a) fo.phi2[a][o] = out[a];
+      }
     }
     if (ANISO)
 #pragma unroll
@@ -479,11 +522,13 @@ int g_fused_slots[2] = {1, 1};
 
 void prepare_fused() {
   const int sa = (int)sizeof(FusedSmemT<true>), si = (int)sizeof(FusedSmemT<false>);
-  cudaFuncSetAttribute(fused_kernel<false, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, si);
-  cudaFuncSetAttribute(fused_kernel<true, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sa);
-  cudaFuncSetAttribute(fused_kernel<true, DM_SL>, cudaFuncAttributeMaxDynamicSharedMemorySize, sa);
-  g_fused_slots[0] = grid_slots(fused_kernel<false, -1>, NTHR, si);
-  g_fused_slots[1] = grid_slots(fused_kernel<true, -1>, NTHR, sa);
+  cudaFuncSetAttribute(fused_kernel<false, -1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, si);
+  cudaFuncSetAttribute(fused_kernel<false, -1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, si);
+  cudaFuncSetAttribute(fused_kernel<true, -1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sa);
+  cudaFuncSetAttribute(fused_kernel<true, -1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sa);
+  cudaFuncSetAttribute(fused_kernel<true, DM_SL, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sa);
+  g_fused_slots[0] = grid_slots(fused_kernel<false, -1, 0>, NTHR, si);
+  g_fused_slots[1] = grid_slots(fused_kernel<true, -1, 0>, NTHR, sa);
 }
 
 void launch_fused(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm, const FusedOut &fo) {
@@ -494,12 +539,18 @@ void launch_fused(cudaStream_t s, const KParams &kp, const BlockView &b, const T
 #endif
   const int kz = chunk_z(b.nz, gx * gy, g_fused_slots[kp.aniso ? 1 : 0], PF_FUSED_WAVES, true);
   dim3 grd(gx, gy, (b.nz + kz - 1) / kz), blk(TX, TY);
+  // shortcuts on: the vote variants, except the solid-liquid anisotropic model
+  // (pf_phi.cu: its vote measured slower in every scenario; bitwise the same)
+  const size_t si = sizeof(FusedSmemT<false>), sa = sizeof(FusedSmemT<true>);
   if (!kp.aniso) {
-    fused_kernel<false, -1><<<grd, blk, sizeof(FusedSmemT<false>), s>>>(tm, kp, b, fo, kz);
+    if (kp.shortcuts) fused_kernel<false, -1, 2><<<grd, blk, si, s>>>(tm, kp, b, fo, kz);
+    else fused_kernel<false, -1, 0><<<grd, blk, si, s>>>(tm, kp, b, fo, kz);
   } else if (kp.dmask == DM_SL) {
-    fused_kernel<true, DM_SL><<<grd, blk, sizeof(FusedSmemT<true>), s>>>(tm, kp, b, fo, kz);
+    fused_kernel<true, DM_SL, 0><<<grd, blk, sa, s>>>(tm, kp, b, fo, kz);
+  } else if (kp.shortcuts) {
+    fused_kernel<true, -1, 2><<<grd, blk, sa, s>>>(tm, kp, b, fo, kz);
   } else {
-    fused_kernel<true, -1><<<grd, blk, sizeof(FusedSmemT<true>), s>>>(tm, kp, b, fo, kz);
+    fused_kernel<true, -1, 0><<<grd, blk, sa, s>>>(tm, kp, b, fo, kz);
   }
 }
 

@@ -1398,8 +1398,7 @@ pf_status enqueue_step(pf_ctx *c, bool graph) {
 // and every state a caller, the window check or the NaN watchdog sees is a
 // complete time level (the run is cut there).  Bitwise the plain sequence.
 bool fusable(const pf_ctx *c) {
-  return c->fusion && c->phi3 && c->p.variant != 1 && (c->p.overlap == 0 || c->p.overlap == 1) && !c->kp.shortcuts &&
-         !c->p.graph;
+  return c->fusion && c->phi3 && c->p.variant != 1 && (c->p.overlap == 0 || c->p.overlap == 1) && !c->p.graph;
 }
 
 // swap phi copy `a` with the third copy: addresses, TMA maps, the phi halo plan

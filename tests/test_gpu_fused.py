@@ -103,6 +103,20 @@ def test_fused_bitwise_blocks_and_calls(pv1):
     _same(ref, _gpu(prm, phi, mu, [1, 3, 2, 4], True))
 
 
+@pytest.mark.parametrize("aniso", [False, True])
+def test_fused_with_shortcuts_bitwise(pgen, aniso):
+    # region shortcuts inside the fused kernel (the vote on phi^{n+1}): bulk
+    # solid below, bulk liquid above, interfaces between — bitwise the plain run
+    pf = _pf()
+    nx, ny, nz = 64, 48, 40
+    cfg, lh, (phi, mu) = _voronoi("c2", nx, ny, nz, lh=16.0)
+    base = dict(nx=nx, ny=ny, layer_height=lh, window=False, aniso=aniso, delta_sl=None)
+    ref = _gpu(pf.make_params(pgen, cfg, **base), phi, mu, [12], False)
+    on = _gpu(pf.make_params(pgen, cfg, shortcuts=True, **base), phi, mu, [12], True, timing=True)
+    assert on[2].fused_launches == 11
+    _same(ref, on)
+
+
 def test_fused_window_forced_shifts_and_nan_cadence(pv1):
     # the front at the trigger height: the window shifts during the run; the
     # fused run is cut before every due window check and NaN check

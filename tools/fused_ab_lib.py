@@ -7,7 +7,7 @@ import torch
 from inputs import gen
 aniso = os.environ.get("ANISO") == "1"
 cfg = gen.load_config("c5" if aniso else "c4"); pd = gen.load_params("v1"); n = 512
-prm = pfm.make_params(pd, cfg, nx=n, ny=n, window=False)
+prm = pfm.make_params(pd, cfg, nx=n, ny=n, window=False, shortcuts=os.environ.get("SHORTCUTS") == "1")
 s = torch.cuda.Stream()
 with pfm.Context(n, n, n, prm, stream=s.cuda_stream) as ctx:
     ctx.set_fusion(os.environ.get("FUSION", "1") == "1")
@@ -17,6 +17,6 @@ with pfm.Context(n, n, n, prm, stream=s.cuda_stream) as ctx:
     ms = e0.elapsed_time(e1) / 20
     ctx.set_timing(True); ctx.step(20)
     inf = ctx.info()
-    print(os.environ.get("PF_LIB", "default"), "aniso" if aniso else "iso", "step", round(ms, 3),
+    print(os.environ.get("PF_LIB", "default"), "aniso" if aniso else "iso", "sc" + os.environ.get("SHORTCUTS", "0"), "step", round(ms, 3),
           "fused", round(inf.ms_fused / max(1, inf.fused_launches), 3),
           "phi", round(inf.ms_phi / max(1, inf.phi_launches), 3), "mu", round(inf.ms_mu / max(1, inf.mu_launches), 3))
