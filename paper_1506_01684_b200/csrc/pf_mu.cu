@@ -7,9 +7,9 @@
 //   * phi^{n+1} tile planes k-1 .. k+2 (interior + ring + corners: the D3C19
 //     stencil of the anti-trapping current needs tangential gradients at face
 //     neighbours) — staged two planes ahead, 4 slots;
-//   * phi^n and mu tile planes k, k+1 — staged one plane ahead, 2 slots;
+//   * phi^n and mu tile planes k .. k+2 — staged two planes ahead, 3 slots;
 //   * table rows; the mobility of plane k (computed once per cell); the x/y
-//     face values of plane k.
+//     face values of plane k (x faces: only the far column; the rest by shuffle).
 // Everything else a face needs (dphi, c^l - c^a, tangential gradients) is
 // derived from the staged planes inside the face routine, and only when the
 // exact-zero guards let the anti-trapping term through.  Flat planes: when the
@@ -28,13 +28,20 @@
 namespace pf {
 
 #ifndef PF_MU_PM_SLOTS
-#define PF_MU_PM_SLOTS 2
+#define PF_MU_PM_SLOTS 3
 #endif
 // phi^n / mu tile slots: 2 = staged one plane ahead, 3 = two planes ahead
 // (measured at 512^3: with 32 x 16 tiles, one CTA per SM, the second plane of
-// lead takes C4 from 3.61 to 3.42 ms, still slower than 32 x 8 tiles with one
-// plane of lead, 3.16; 32 x 8 with three slots no longer fits 2 CTAs per SM: 4.74)
+// lead takes C4 from 3.61 to 3.42 ms; 32 x 8 with three slots fits 2 CTAs per SM
+// only since the x faces travel by shuffle (kShfl, 4 KB less): C4 3.08 -> 2.97 ms)
 constexpr int NPM = PF_MU_PM_SLOTS;
+// x faces: with TX = 32 a warp is one tile row, so the +x face of a cell is the
+// own -x face of the next lane (a shuffle) and shared memory keeps only the
+// tile's far column (the +x faces of the last lane): 4 KB less per CTA
+#ifndef PF_MU_SHFL
+#define PF_MU_SHFL 1
+#endif
+constexpr bool kShfl = PF_MU_SHFL != 0 && TX == 32;
 
 struct __align__(128) MuSmem {
   double pn[NSLOT][NPH][TSZ];     // phi^{n+1}, planes k-1 .. k+2
@@ -42,7 +49,7 @@ struct __align__(128) MuSmem {
   double mu[NPM][NMU][TSZ];       // mu^n
   double tab[NSLOT][TAB];
   double M[NMU][RY][RX];          // mobility of plane k
-  double fx[NMU][TY][TX + 1];     // x-face values at i - 1/2
+  double fx[NMU][TY][kShfl ? 1 : TX + 1];   // x-face values at i - 1/2 (kShfl: the far column i = TX only)
   double fy[NMU][TY + 1][TX];     // y-face values at j - 1/2
   uint64_t bar_pn[NSLOT];         // phi^{n+1} + table of a plane
   uint64_t bar_pm[NPM];           // phi^n + mu of a plane
@@ -65,6 +72,7 @@ constexpr int kMuUnroll = PF_MU_UNROLL;   // plane-loop unroll (round 1: 2 -> 4 
 constexpr int NBOX = RX * RY;     // staged cells of a plane tile (interior + ring + corners)
 static_assert(NBOX <= 2 * NTHR, "flatness check covers the box in two passes");
 #define T(arr, row, col) TILE_AT(arr, row, col)
+#define FX_FAR(c, r) S.fx[c][r][kShfl ? 0 : TX]
 constexpr uint32_t MU_PN_BYTES = (NPH * RXS * RY + TAB) * 8;   // phi^{n+1} tiles + table row
 constexpr uint32_t MU_PM_BYTES = ((NPH + NMU) * RXS * RY) * 8;  // phi^n + mu tiles
 
@@ -296,13 +304,13 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
     if (fast_xy && MODE == MU_NEIGHBOR) {   // J = 0 on every x/y face of the plane
 #pragma unroll
       for (int c = 0; c < NMU; ++c) {
-        S.fx[c][ty][tx] = 0.0;
+        if (!kShfl) S.fx[c][ty][tx] = 0.0;
         S.fy[c][ty][tx] = 0.0;
       }
       if (tid < TX + TY) {
 #pragma unroll
         for (int c = 0; c < NMU; ++c) {
-          if (tid >= TX) S.fx[c][tid - TX][TX] = 0.0;
+          if (tid >= TX) FX_FAR(c, tid - TX) = 0.0;
           else S.fy[c][TY][tid] = 0.0;
         }
       }
@@ -311,7 +319,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
       for (int c = 0; c < NMU; ++c) {   // own mu, M from registers (inb: the staged values)
         fxo[c] = mu_flux_diff(kp, S.M[c][orow][oc - 1], Mown[c], T(S.mu[s2][c], orow, oc - 1), mu_c[c]);
         fyo[c] = mu_flux_diff(kp, S.M[c][orow - 1][oc], Mown[c], T(S.mu[s2][c], orow - 1, oc), mu_c[c]);
-        S.fx[c][ty][tx] = fxo[c];
+        if (!kShfl) S.fx[c][ty][tx] = fxo[c];
         S.fy[c][ty][tx] = fyo[c];
       }
       if (tid < TX + TY) {
@@ -322,7 +330,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
         for (int c = 0; c < NMU; ++c) {
           const double f = mu_flux_diff(kp, S.M[c][r0][c0], S.M[c][r1][c1], T(S.mu[s2][c], r0, c0),
                                         T(S.mu[s2][c], r1, c1));
-          if (d == 0) S.fx[c][r0 - 1][TX] = f;
+          if (d == 0) FX_FAR(c, r0 - 1) = f;
           else S.fy[c][TY][c0 - 1] = f;
         }
       }
@@ -333,8 +341,10 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
         lo.Mv[0] = S.M[0][orow][oc - 1]; lo.Mv[1] = S.M[1][orow][oc - 1];
         hi.Mv[0] = Mown[0]; hi.Mv[1] = Mown[1];
         mu_face_t<MODE == MU_FULL, kMuRoll>(kp, lo, hi, 0, fxo);
-        S.fx[0][ty][tx] = fxo[0];
-        S.fx[1][ty][tx] = fxo[1];
+        if (!kShfl) {
+          S.fx[0][ty][tx] = fxo[0];
+          S.fx[1][ty][tx] = fxo[1];
+        }
       }
       {  // own -y face
         RawQ lo = rawq(k, oc, orow - 1), hi = rawq(k, oc, orow);
@@ -352,7 +362,7 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
         lo.Mv[0] = S.M[0][r0][c0]; lo.Mv[1] = S.M[1][r0][c0];
         hi.Mv[0] = S.M[0][r1][c1]; hi.Mv[1] = S.M[1][r1][c1];
         mu_face_t<MODE == MU_FULL, kMuRoll>(kp, lo, hi, d, f);
-        if (d == 0) { S.fx[0][r0 - 1][TX] = f[0]; S.fx[1][r0 - 1][TX] = f[1]; }
+        if (d == 0) { FX_FAR(0, r0 - 1) = f[0]; FX_FAR(1, r0 - 1) = f[1]; }
         else { S.fy[0][TY][c0 - 1] = f[0]; S.fy[1][TY][c0 - 1] = f[1]; }
       }
     }
@@ -382,9 +392,10 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
     }
     // the divergence's own-face part before the barrier (the oracle's O5.9
     // sum in another order: equal up to rounding)
-    double dpart[NMU];
+    double dpart[NMU], fxp[NMU];   // fxp: the +x face from the next lane (kShfl)
 #pragma unroll
     for (int c = 0; c < NMU; ++c) {
+      fxp[c] = kShfl ? __shfl_down_sync(0xffffffffu, fxo[c], 1) : 0.0;
       dpart[c] = ((fzp[c] - fzm[c]) - fxo[c]) - fyo[c];
       fzm[c] = fzp[c];
       Mown[c] = Mnx[c];
@@ -394,7 +405,9 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
     if (active) {
       double divf[NMU], out[NMU];
 #pragma unroll
-      for (int c = 0; c < NMU; ++c) divf[c] = dpart[c] + (S.fx[c][ty][tx + 1] + S.fy[c][ty + 1][tx]);
+      for (int c = 0; c < NMU; ++c)
+        divf[c] = dpart[c] + ((kShfl ? (tx == TX - 1 ? FX_FAR(c, ty) : fxp[c]) : S.fx[c][ty][tx + 1]) +
+                              S.fy[c][ty + 1][tx]);
       const int64_t o = (int64_t)k * b.plane + colo;
       if (MODE != MU_NEIGHBOR) {
         mu_cell_update(kp, S.tab[sn], po_c, pn_c, mu_c, divf, out);
