@@ -167,6 +167,7 @@ __global__ void __launch_bounds__(NTHR, PF_FUSED_MINB)
     const uint32_t f = (__all_sync(0xffffffffu, one) ? 1u : 0u) | (__all_sync(0xffffffffu, zero) ? 2u : 0u);
     if ((tid & 31) == 0) S.wflat[e][tid >> 5] = f;
   };
+  // (a REDUX over the warps' votes as in pf_mu.cu measured +0.4 % here)
   auto read_flat = [&](int e) {
     uint32_t f = 3u;
 #pragma unroll

@@ -181,7 +181,14 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
     const uint32_t f = (__all_sync(0xffffffffu, one) ? 1u : 0u) | (__all_sync(0xffffffffu, zero) ? 2u : 0u);
     if ((tid & 31) == 0) S.wflat[e][tid >> 5] = f;
   };
+  // the AND of the warps' votes: lane l reads warp (l mod nwarps)'s, one
+  // warp-wide AND reduction (REDUX) instead of a load per warp in every thread
+  // (measured: C4 mu 2.971 -> 2.957 ms)
+#ifndef PF_FLAT_REDUX
+#define PF_FLAT_REDUX 1
+#endif
   auto read_flat = [&](int e) {
+    if (PF_FLAT_REDUX) return __reduce_and_sync(0xffffffffu, S.wflat[e][(tid & 31) % (NTHR / 32)]);
     uint32_t f = 3u;
 #pragma unroll
     for (int w = 0; w < NTHR / 32; ++w) f &= S.wflat[e][w];
