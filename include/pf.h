@@ -296,8 +296,8 @@ pf_status pf_set_shortcuts(pf_ctx *c, int32_t on);
  * with bitwise the same results): measured at 512^3 the
  * isotropic step is 3 % faster fused, the anisotropic one 19 % slower (its
  * fused kernel is register-bound).
- * The first call with on = 1 allocates a third phi copy (4 doubles per cell
- * of the block, ghosts and window slack included).
+ * on = 1 allocates a third phi copy (4 doubles per cell of the block, ghosts
+ * and window slack included); on = 0 releases it.
  * Errors: PF_ERR_ARG (NULL), PF_ERR_STATE after an error, PF_ERR_CUDA if that
  * copy does not fit (fusion stays off; the context stays usable). */
 pf_status pf_set_fusion(pf_ctx *c, int32_t on);

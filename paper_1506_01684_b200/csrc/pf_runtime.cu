@@ -1799,6 +1799,19 @@ pf_status pf_set_fusion(pf_ctx *c, int32_t on) {
     for (auto &b : c->blocks) CKS(encode_maps(c, b));
     CKS(build_plans(c));
   }
+  if (!on && c->phi3) {   // off releases the third phi copy and the second table
+    CKS(join_mu(c));
+    CK(cudaStreamSynchronize(c->stream));
+    for (auto &b : c->blocks)
+      for (int a = 0; a < NPH; ++a) { cudaFree(b.phi[2][a]); b.phi[2][a] = nullptr; }
+    Plan &pl = c->plan[0][2];
+    if (pl.d_local) cudaFree(pl.d_local);
+    if (pl.d_unpack) cudaFree(pl.d_unpack);
+    pl = Plan{};
+    cudaFree(c->d_tab2);
+    c->d_tab2 = nullptr;
+    c->phi3 = false;
+  }
   c->fusion = on != 0;
   return PF_OK;
 }

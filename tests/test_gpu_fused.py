@@ -101,6 +101,14 @@ def test_fused_bitwise_blocks_and_calls(pv1):
     ref = _gpu(prm, phi, mu, [10], False)
     _same(ref, _gpu(prm, phi, mu, [10], True, blocks=(2, 2, 1)))
     _same(ref, _gpu(prm, phi, mu, [1, 3, 2, 4], True))
+    # fusion switched off (the third copy released) and on again mid-run
+    pf = _pf()
+    with pf.Context(48, 40, 30, prm) as ctx:
+        ctx.write(phi, mu)
+        for on, n in ((True, 3), (False, 2), (True, 5)):
+            ctx.set_fusion(on)
+            ctx.step(n)
+        _same(ref, ctx.read())
 
 
 @pytest.mark.parametrize("aniso", [False, True])
