@@ -429,34 +429,12 @@ __device__ __forceinline__ void phi_cell_project(const KParams &kp, const double
   // such that u_j > t_j.  Since t_{j+1} - t_j = (u_{j+1} - t_j)/(j+1), t_j
   // rises while j < rho and falls after, so theta = max_j t_j: a max tree
   // instead of a chain of dependent selects (same value up to rounding ties).
-#ifndef PF_INT_SORT
-#define PF_INT_SORT 0
-#endif
-#if PF_INT_SORT
-  // the sort network and the max tree on order-preserving integer keys of the
-  // doubles (sign-magnitude -> two's complement: k = i ^ ((i >> 63) & 0x7f..f),
-  // an involution): integer-pipe instructions instead of DSETP / DMNMX
-  auto key = [](double v) {
-    const long long i = __double_as_longlong(v);
-    return i ^ ((i >> 63) & 0x7fffffffffffffffll);
-  };
-  auto unkey = [](long long k) { return __longlong_as_double(k ^ ((k >> 63) & 0x7fffffffffffffffll)); };
-  long long k0 = key(x[0]), k1 = key(x[1]), k2 = key(x[2]), k3 = key(x[3]), kt;
-#define PF_CSWAP(p, q) { kt = p < q ? q : p; q = p < q ? p : q; p = kt; }
-  PF_CSWAP(k0, k1) PF_CSWAP(k2, k3) PF_CSWAP(k0, k2) PF_CSWAP(k1, k3) PF_CSWAP(k1, k2)
-#undef PF_CSWAP
-  const double u0 = unkey(k0), u1 = unkey(k1), u2 = unkey(k2), u3 = unkey(k3);
-  const double c1 = u0 - 1.0, c2 = c1 + u1, c3 = c2 + u2, c4 = c3 + u3;
-  const long long m = max(max(key(c1), key(0.5 * c2)), max(key(c3 * (1.0 / 3.0)), key(0.25 * c4)));
-  const double theta = unkey(m);
-#else
   double u0 = x[0], u1 = x[1], u2 = x[2], u3 = x[3], t;
 #define PF_CSWAP(p, q) if (p < q) { t = p; p = q; q = t; }
   PF_CSWAP(u0, u1) PF_CSWAP(u2, u3) PF_CSWAP(u0, u2) PF_CSWAP(u1, u3) PF_CSWAP(u1, u2)
 #undef PF_CSWAP
   const double c1 = u0 - 1.0, c2 = c1 + u1, c3 = c2 + u2, c4 = c3 + u3;
   const double theta = fmax(fmax(c1, 0.5 * c2), fmax(c3 * (1.0 / 3.0), 0.25 * c4));
-#endif
   // out = max(d, 0) on the integer pipe: every bit of a negative d cleared
   // (a double compare is an FP64-pipe instruction, the sweep's bottleneck:
   // measured -1.7 % phi time); -0 gives +0, a NaN keeps its sign's rule
