@@ -52,6 +52,8 @@ def rank_main(r):
     try:
         c = pf.Context(NX, NY, NZ, prm, px, py, pz, rank=r, nranks=N, device=0, nccl_id=nid)
         ctxs[r] = c
+        if spec.get("fusion"):   # fused mu(n) + phi(n+1) kernels; the reference runs the separate sweeps
+            c.set_fusion(True)
         inf = c.info()
         x0, y0, z0 = int(inf.x0), int(inf.y0), int(inf.z0)
         nz, ny, nx = c.shape

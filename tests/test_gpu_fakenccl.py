@@ -48,6 +48,21 @@ def test_ranks_overlap_modes(fakelib, overlap):
     assert out["equal_phi"] and out["equal_mu"]
 
 
+@pytest.mark.parametrize("blocks", [(2, 1, 1), (2, 2, 2)])
+def test_ranks_fused_bitwise_equal_single_context(fakelib, blocks):
+    # every rank with fused steps (both ghost exchanges after each fused kernel,
+    # over the NCCL stand-in) against one context with the separate sweeps
+    out = _run(fakelib, grid=[32, 24, 20], blocks=list(blocks), steps=12, layer_height=9.5, fusion=True)
+    assert out["equal_phi"] and out["equal_mu"] and out["moved"] > 1e-3
+
+
+def test_ranks_fused_window_aniso(fakelib):
+    out = _run(fakelib, grid=[24, 24, 24], blocks=[2, 2, 2], steps=30, window=True, config="c5",
+               layer_height=17.5, aniso=True, fusion=True)
+    assert out["equal_phi"] and out["equal_mu"]
+    assert out["ref_shifts"] > 0 and out["shifts"] == [out["ref_shifts"]] * 8
+
+
 def test_ranks_step_io(fakelib):
     out = _run(fakelib, grid=[32, 24, 20], blocks=[2, 1, 2], steps=6, step_io=True, layer_height=9.5)
     assert out["equal_phi"] and out["equal_mu"]
