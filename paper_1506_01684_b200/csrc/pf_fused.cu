@@ -36,7 +36,13 @@ namespace {
 #ifndef PF_FUSED_PM_SLOTS
 #define PF_FUSED_PM_SLOTS 2
 #endif
-constexpr int FPM = PF_FUSED_PM_SLOTS;   // phi^n / mu slots: planes k .. k+FPM-1 (staged FPM-1 ahead)
+constexpr int FPM = PF_FUSED_PM_SLOTS;
+// mu x faces: the +x face of a cell is the own -x face of the next lane in its
+// TX-wide row segment of the warp (shuffle); shared memory keeps the far column
+#ifndef PF_FUSED_SHFL
+#define PF_FUSED_SHFL 0
+#endif
+constexpr bool kFShfl = PF_FUSED_SHFL != 0 && (TX == 16 || TX == 32);   // phi^n / mu slots: planes k .. k+FPM-1 (staged FPM-1 ahead)
 // (3 slots measured slower: 7.67 vs 6.33 ms at 512^3 — the extra 6.6 KB costs the third CTA per SM)
 template <bool ANISO>
 struct __align__(128) FusedSmemT {
@@ -46,7 +52,7 @@ struct __align__(128) FusedSmemT {
   double tab[NSLOT][TAB];         // table rows of step n (mu part)
   double tabp[NSLOT][TAB];        // table rows of step n+1 (phi part)
   double M[NMU][RY][RX];          // mobility of plane k
-  double fx[NMU][TY][TX + 1];     // mu x-face values at i - 1/2
+  double fx[NMU][TY][kFShfl ? 1 : TX + 1];   // mu x-face values at i - 1/2 (kFShfl: the far column only)
   double fy[NMU][TY + 1][TX];     // mu y-face values at j - 1/2
   double pfx[NPH][TY][TX + 1];    // phi x-face fluxes
   double pfy[NPH][TY + 1][TX];    // phi y-face fluxes
@@ -305,7 +311,7 @@ __global__ void __launch_bounds__(NTHR, PF_FUSED_MINB)
       for (int c = 0; c < NMU; ++c) {
         fxo[c] = mu_flux_diff(kp, S.M[c][orow][oc - 1], Mown[c], T(S.mu[s2][c], orow, oc - 1), mu_c[c]);
         fyo[c] = mu_flux_diff(kp, S.M[c][orow - 1][oc], Mown[c], T(S.mu[s2][c], orow - 1, oc), mu_c[c]);
-        S.fx[c][ty][tx] = fxo[c];
+        if (!kFShfl) S.fx[c][ty][tx] = fxo[c];
         S.fy[c][ty][tx] = fyo[c];
       }
       if (tid < TX + TY) {
@@ -316,7 +322,7 @@ __global__ void __launch_bounds__(NTHR, PF_FUSED_MINB)
         for (int c = 0; c < NMU; ++c) {
           const double f = mu_flux_diff(kp, S.M[c][r0][c0], S.M[c][r1][c1], T(S.mu[s2][c], r0, c0),
                                         T(S.mu[s2][c], r1, c1));
-          if (d == 0) S.fx[c][r0 - 1][TX] = f;
+          if (d == 0) S.fx[c][r0 - 1][kFShfl ? 0 : TX] = f;
           else S.fy[c][TY][c0 - 1] = f;
         }
       }
@@ -327,8 +333,10 @@ __global__ void __launch_bounds__(NTHR, PF_FUSED_MINB)
         lo.Mv[0] = S.M[0][orow][oc - 1]; lo.Mv[1] = S.M[1][orow][oc - 1];
         hi.Mv[0] = Mown[0]; hi.Mv[1] = Mown[1];
         mu_face_t<true, true>(kp, lo, hi, 0, fxo);
-        S.fx[0][ty][tx] = fxo[0];
-        S.fx[1][ty][tx] = fxo[1];
+        if (!kFShfl) {
+          S.fx[0][ty][tx] = fxo[0];
+          S.fx[1][ty][tx] = fxo[1];
+        }
       }
       {
         auto lo = rawq(k, oc, orow - 1), hi = rawq(k, oc, orow);
@@ -346,7 +354,7 @@ __global__ void __launch_bounds__(NTHR, PF_FUSED_MINB)
         lo.Mv[0] = S.M[0][r0][c0]; lo.Mv[1] = S.M[1][r0][c0];
         hi.Mv[0] = S.M[0][r1][c1]; hi.Mv[1] = S.M[1][r1][c1];
         mu_face_t<true, true>(kp, lo, hi, d, f);
-        if (d == 0) { S.fx[0][r0 - 1][TX] = f[0]; S.fx[1][r0 - 1][TX] = f[1]; }
+        if (d == 0) { S.fx[0][r0 - 1][kFShfl ? 0 : TX] = f[0]; S.fx[1][r0 - 1][kFShfl ? 0 : TX] = f[1]; }
         else { S.fy[0][TY][c0 - 1] = f[0]; S.fy[1][TY][c0 - 1] = f[1]; }
       }
     }
@@ -366,9 +374,10 @@ __global__ void __launch_bounds__(NTHR, PF_FUSED_MINB)
     }
 #pragma unroll
     for (int a = 0; a < NPH; ++a) pn_c[a] = T(S.pn[sn][a], orow, oc);
-    double dpart[NMU];
+    double dpart[NMU], fxp[NMU];   // fxp: the +x face from the next lane (kFShfl)
 #pragma unroll
     for (int c = 0; c < NMU; ++c) {
+      fxp[c] = kFShfl ? __shfl_down_sync(0xffffffffu, fxo[c], 1, TX) : 0.0;
       dpart[c] = ((fzp[c] - fzm[c]) - fxo[c]) - fyo[c];
       fzm[c] = fzp[c];
       Mown[c] = Mnx[c];
@@ -482,7 +491,9 @@ __global__ void __launch_bounds__(NTHR, PF_FUSED_MINB)
     if (active) {
       double divf[NMU], mu1[NMU];
 #pragma unroll
-      for (int c = 0; c < NMU; ++c) divf[c] = dpart[c] + (S.fx[c][ty][tx + 1] + S.fy[c][ty + 1][tx]);
+      for (int c = 0; c < NMU; ++c)
+        divf[c] = dpart[c] + ((kFShfl ? (tx == TX - 1 ? S.fx[c][ty][0] : fxp[c]) : S.fx[c][ty][tx + 1]) +
+                              S.fy[c][ty + 1][tx]);
       const int64_t o = (int64_t)k * b.plane + colo;
       mu_cell_update(kp, S.tab[sn], po_c, pn_c, mu_c, divf, mu1);
       b.out[0][o] = mu1[0];
