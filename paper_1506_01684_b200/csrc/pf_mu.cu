@@ -446,7 +446,15 @@ void prepare_mu_tiled() {
 template <int MODE>
 void launch_mu_mode(cudaStream_t s, const KParams &kp, const BlockView &b, const TmaMaps &tm) {
   const int gx = (b.nx + TX - 1) / TX, gy = (b.ny + TY - 1) / TY;
-  const int kz = chunk_z(b.nz, gx * gy, g_mu_slots, 8, true);
+// >= 8 waves or a >= 97 % full last one: 256-plane chunks at 512^3 (measured
+// with the two-plane lead: 256 -> 2.958 ms, 128 -> 2.966, 64 -> 2.995, 32 -> 3.059)
+#ifndef PF_MU_WAVES
+#define PF_MU_WAVES 8
+#endif
+  int kz = chunk_z(b.nz, gx * gy, g_mu_slots, PF_MU_WAVES, true);
+#ifdef PF_MU_KZ
+  kz = std::min(kz, PF_MU_KZ);
+#endif
   dim3 grd(gx, gy, (b.nz + kz - 1) / kz), blk(TX, TY);
   mu_tiled_kernel<MODE><<<grd, blk, sizeof(MuSmem), s>>>(tm, kp, b, kz);
 }
