@@ -152,3 +152,34 @@ def test_fused_vs_oracle(pv1):
     g = _gpu(prm, phi, mu, [100], True)
     o = O.run(op, phi, mu, 100)
     assert O.rel_maxnorm(g[0], o[0]) <= TOL100 and O.rel_maxnorm(g[1], o[1]) <= TOL100
+
+
+@pytest.mark.parametrize("name,shape,steps,lh", [
+    ("c3", (256, 128, 96), 100, 64.6),     # lamellar + window, front at the trigger: forced shifts
+    ("c4", (256, 256, 256), 100, None),    # Voronoi, C4's recipe at 256^3
+    ("c5", (256, 256, 256), 100, None),    # anisotropic (solid-liquid mask) + window
+    ("c4", (512, 512, 512), 12, None),     # C4 at its bench size and launch configuration
+])
+def test_fused_bitwise_config_replicas(pv1, name, shape, steps, lh):
+    # every config's features over a long run (or at full size): fused == separate, bit for bit
+    pf = _pf()
+    nx, ny, nz = shape
+    cfg = gen.load_config(name)
+    prm = pf.make_params(pv1, cfg, nx=nx, ny=ny, **({"layer_height": lh} if lh else {}))
+    res = []
+    for fusion in (False, True):
+        with pf.Context(nx, ny, nz, prm) as ctx:
+            ctx.set_fusion(fusion)
+            if lh:   # the generator's state with the front moved up to the window trigger
+                spec = gen.spec_from_config(cfg, nx, ny)
+                spec.layer_height = lh
+                ctx.write(*gen.generate(spec, nx, ny, nz))
+            else:
+                ctx.init(cfg["seed"])
+            ctx.step(steps)
+            inf = ctx.info()
+            phi, mu = ctx.read()
+            res.append((phi[:, ::3], mu[:, ::3], inf.shifts, inf.z_origin))
+    (p0, m0, s0, z0), (p1, m1, s1, z1) = res
+    assert s0 == s1 and z0 == z1 and (name != "c3" or s0 > 0)
+    assert np.array_equal(p0, p1) and np.array_equal(m0, m1)
