@@ -33,6 +33,18 @@ __host__ __device__ constexpr int pair_of(int a, int b) {
   return a < b ? (a == 0 ? b - 1 : a + b) : (b == 0 ? a - 1 : a + b);
 }
 
+// Output stores of the sweeps: the fields are gigabytes, never re-read from L2
+// by the next kernel, so they are written with the evict-first (streaming)
+// policy and leave L2 to the tile rings neighbouring CTAs re-read (measured at
+// 512^3: the sweeps unchanged within 0.05 %, the fused kernel -0.4 %)
+#ifndef PF_STCS
+#define PF_STCS 1
+#endif
+__device__ __forceinline__ void st_field(double *p, double v) {
+  if (PF_STCS) __stcs(p, v);
+  else *p = v;
+}
+
 // Per-step constants (kernel argument, lives in the constant bank).
 struct KParams {
   double dt, inv_dt, inv_dx, inv_2dx;

@@ -496,11 +496,11 @@ __global__ void __launch_bounds__(NTHR, PF_FUSED_MINB)
                               S.fy[c][ty + 1][tx]);
       const int64_t o = (int64_t)k * b.plane + colo;
       mu_cell_update(kp, S.tab[sn], po_c, pn_c, mu_c, divf, mu1);
-      b.out[0][o] = mu1[0];
-      b.out[1][o] = mu1[1];
+      st_field(&b.out[0][o], mu1[0]);
+      st_field(&b.out[1][o], mu1[1]);
       if (SC == 2 && skip) {
 #pragma unroll
-        for (int a = 0; a < NPH; ++a) fo.phi2[a][o] = pn_c[a];
+        for (int a = 0; a < NPH; ++a) st_field(&fo.phi2[a][o], pn_c[a]);
       } else {
       const double *tp = S.tabp[sn];
       double r0[NPH], q[NPH];
@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(NTHR, PF_FUSED_MINB)
       for (int a = 0; a < NPH; ++a) rhs[a] = q[a] - c * (S.pfx[a][ty][tx + 1] + S.pfy[a][ty + 1][tx]);
       phi_cell_project(kp, pn_c, rhs, out);
 #pragma unroll
-      for (int a = 0; a < NPH; ++a) fo.phi2[a][o] = out[a];
+      for (int a = 0; a < NPH; ++a) st_field(&fo.phi2[a][o], out[a]);
       }
     }
     if (ANISO)

@@ -418,13 +418,13 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
       const int64_t o = (int64_t)k * b.plane + colo;
       if (MODE != MU_NEIGHBOR) {
         mu_cell_update(kp, S.tab[sn], po_c, pn_c, mu_c, divf, out);
-        b.out[0][o] = out[0];
-        b.out[1][o] = out[1];
+        st_field(&b.out[0][o], out[0]);
+        st_field(&b.out[1][o], out[1]);
       } else if (divf[0] != 0.0 || divf[1] != 0.0) {   // divj = 0: mu_loc stands, bit for bit
         const double loc[NMU] = {b.out[0][o], b.out[1][o]};
         mu_cell_add_j(kp, S.tab[sn], pn_c, loc, divf, out);
-        b.out[0][o] = out[0];
-        b.out[1][o] = out[1];
+        st_field(&b.out[0][o], out[0]);
+        st_field(&b.out[1][o], out[1]);
       }
     }
   }

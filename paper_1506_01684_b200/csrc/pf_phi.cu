@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(NTHR, ANISO ? PF_PHI_MINB : PF_PHI_MINB_ISO)
     if (active && skip) {
       const int64_t o = (int64_t)k * b.plane + colo;
 #pragma unroll
-      for (int a = 0; a < NPH; ++a) b.out[a][o] = pc[a];
+      for (int a = 0; a < NPH; ++a) st_field(&b.out[a][o], pc[a]);
     } else if (active) {
       const double c = S.tab[sc][ANISO ? T_EPSTDX16 : T_EPSTDX];   // anisotropic fluxes: 16 dx j
       if (ANISO) {
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(NTHR, ANISO ? PF_PHI_MINB : PF_PHI_MINB_ISO)
       phi_cell_project(kp, pc, rhs, out);
       const int64_t o = (int64_t)k * b.plane + colo;
 #pragma unroll
-      for (int a = 0; a < NPH; ++a) b.out[a][o] = out[a];
+      for (int a = 0; a < NPH; ++a) st_field(&b.out[a][o], out[a]);
     }
     if (ANISO)
 #pragma unroll
