@@ -183,3 +183,21 @@ def test_fused_bitwise_config_replicas(pv1, name, shape, steps, lh):
     (p0, m0, s0, z0), (p1, m1, s1, z1) = res
     assert s0 == s1 and z0 == z1 and (name != "c3" or s0 > 0)
     assert np.array_equal(p0, p1) and np.array_equal(m0, m1)
+
+
+def test_fused_then_step_io(pv1):
+    # pf_step_io after fused runs (the phi copies have rotated: its slab copy
+    # lists are rebuilt for the new addresses) and fused runs after it
+    pf = _pf()
+    cfg, lh, (phi, mu) = _voronoi("c2", 40, 36, 64, lh=20.0)
+    prm = pf.make_params(pv1, cfg, nx=40, ny=36, layer_height=lh, window=False)
+    ref = _gpu(prm, phi, mu, [12], False)
+    with pf.Context(40, 36, 64, prm) as ctx:
+        ctx.set_fusion(True)
+        ctx.write(phi, mu)
+        ctx.step(4)
+        p, m = ctx.step_io(*ctx.read())   # step 5 through the slab pipeline
+        ctx.step(3)
+        p, m = ctx.step_io(p, m)          # step 9 (the rotation has moved on)
+        ctx.step(3)
+        _same(ref, ctx.read())
