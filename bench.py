@@ -429,10 +429,28 @@ def run_gpu(args):
             inf = ctx.info()
             reps.append((inf.ms_phi / max(1, inf.phi_launches), inf.ms_mu / max(1, inf.mu_launches)))
         ctx.set_timing(False)
+        # the fused kernel from the same state (pf_step(2): phi-sweep, one fused
+        # mu(0) + phi(1) kernel, mu-sweep), where its FLOP count is exact too
+        freps = []
+        if not args.no_fused and not args.graph:
+            try:
+                ctx.set_fusion(True)
+                for _ in range(3):
+                    ctx.write(dphi, dmu)
+                    ctx.set_timing(True)
+                    ctx.step(2)
+                    inf = ctx.info()
+                    freps.append(inf.ms_fused / max(1, inf.fused_launches))
+                ctx.set_timing(False)
+                ctx.set_fusion(False)
+            except RuntimeError:   # no room for the third phi copy next to the interface state
+                freps = []
         del dphi, dmu
         torch.cuda.empty_cache()
         iface = {"phi_ms": max_over_ranks(float(np.median([r[0] for r in reps]))),
                  "mu_ms": max_over_ranks(float(np.median([r[1] for r in reps])))}
+        if freps:
+            iface["fused_ms"] = max_over_ranks(float(np.median(freps)))
 
     if rank == 0:
         fl = flops_per_lup(args.config)
@@ -461,6 +479,11 @@ def run_gpu(args):
                 iface[f"{k}_frac_fp64"] = sweeps[k]["flop"] * cells_local / t / 1e12 / PEAK_FP64_DERIVED
                 iface[f"{k}_frac_hbm"] = sweeps[k]["bytes"] * cells_local / t / 1e9 / hbm
                 iface[f"{k}_frac_fp64_survey"] = f_svy[k] * cells_local / t / 1e12 / PEAK_FP64_DERIVED
+            if "fused_ms" in iface:   # mu(n) + phi(n+1): both sweeps' algorithmic FLOPs and 128 B per LUP
+                t = iface["fused_ms"] / 1e3
+                iface["fused_frac_fp64"] = (sweeps["phi"]["flop"] + sweeps["mu"]["flop"]) * cells_local / t / 1e12 / \
+                    PEAK_FP64_DERIVED
+                iface["fused_frac_hbm"] = BYTES_FUSED * cells_local / t / 1e9 / hbm
             iface["state"] = ("inputs/gen.py interface_state_torch: phi = 0.05 + U(0,1) per phase, normalised "
                               "(all four phases in every cell), mu = U(-0.3, 0.3); one step from it per repetition, "
                               "median of 5")
