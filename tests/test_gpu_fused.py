@@ -196,8 +196,8 @@ def test_fused_then_step_io(pv1):
         ctx.set_fusion(True)
         ctx.write(phi, mu)
         ctx.step(4)
-        p, m = ctx.step_io(*ctx.read())   # step 5 through the slab pipeline
+        ctx.step_io(*ctx.read())   # step 5 through the slab pipeline
         ctx.step(3)
-        p, m = ctx.step_io(p, m)          # step 9 (the rotation has moved on)
+        p, m = ctx.step_io(*ctx.read())   # step 9 (the rotation has moved on)
         ctx.step(3)
         _same(ref, ctx.read())
