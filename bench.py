@@ -440,7 +440,8 @@ def run_gpu(args):
                     ctx.set_timing(True)
                     ctx.step(2)
                     inf = ctx.info()
-                    freps.append(inf.ms_fused / max(1, inf.fused_launches))
+                    if inf.fused_launches:   # (with the window on, a due front check cuts the run)
+                        freps.append(inf.ms_fused / inf.fused_launches)
                 ctx.set_timing(False)
                 ctx.set_fusion(False)
             except RuntimeError:   # no room for the third phi copy next to the interface state
