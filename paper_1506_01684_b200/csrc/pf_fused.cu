@@ -47,7 +47,7 @@ constexpr bool kFShfl = PF_FUSED_SHFL != 0 && (TX == 16 || TX == 32);   // phi^n
 template <bool ANISO>
 struct __align__(128) FusedSmemT {
   double pn[NSLOT][NPH][TSZ];     // phi^{n+1}, planes k-1 .. k+2
-  double po[FPM][NPH][TSZ];       // phi^n, planes k, k+1
+  double po[FPM][NPH][TSZ];       // phi^n, planes k .. k+FPM-1
   double mu[FPM][NMU][TSZ];       // mu^n
   double tab[NSLOT][TAB];         // table rows of step n (mu part)
   double tabp[NSLOT][TAB];        // table rows of step n+1 (phi part)
