@@ -110,6 +110,12 @@ struct FColQ {
 #endif
 // plane-loop unroll (measured at 512^3, isotropic: 1 -> 6.36 ms, 2 -> 6.45, 4 -> 7.41)
 constexpr int kFusedUnroll = PF_FUSED_UNROLL;
+// the three solids of an x/y face's anti-trapping current in a rolled loop (1) or unrolled (0), as pf_mu.cu
+// (here the rolled loop measured faster: 6.31 vs 6.40 ms at 512^3 — the fused kernel's code is twice the size)
+#ifndef PF_FUSED_ROLL
+#define PF_FUSED_ROLL 1
+#endif
+constexpr bool kFRoll = PF_FUSED_ROLL != 0;
 // 3 CTAs of 128 threads per SM (166 registers; 2 CTAs: 7.78 ms vs 6.45)
 #ifndef PF_FUSED_MINB
 #define PF_FUSED_MINB (384 / NTHR)
@@ -332,7 +338,7 @@ __global__ void __launch_bounds__(NTHR, PF_FUSED_MINB)
         auto lo = rawq(k, oc - 1, orow), hi = rawq(k, oc, orow);
         lo.Mv[0] = S.M[0][orow][oc - 1]; lo.Mv[1] = S.M[1][orow][oc - 1];
         hi.Mv[0] = Mown[0]; hi.Mv[1] = Mown[1];
-        mu_face_t<true, true>(kp, lo, hi, 0, fxo);
+        mu_face_t<true, kFRoll>(kp, lo, hi, 0, fxo);
         if (!kFShfl) {
           S.fx[0][ty][tx] = fxo[0];
           S.fx[1][ty][tx] = fxo[1];
@@ -342,7 +348,7 @@ __global__ void __launch_bounds__(NTHR, PF_FUSED_MINB)
         auto lo = rawq(k, oc, orow - 1), hi = rawq(k, oc, orow);
         lo.Mv[0] = S.M[0][orow - 1][oc]; lo.Mv[1] = S.M[1][orow - 1][oc];
         hi.Mv[0] = Mown[0]; hi.Mv[1] = Mown[1];
-        mu_face_t<true, true>(kp, lo, hi, 1, fyo);
+        mu_face_t<true, kFRoll>(kp, lo, hi, 1, fyo);
         S.fy[0][ty][tx] = fyo[0];
         S.fy[1][ty][tx] = fyo[1];
       }
@@ -353,7 +359,7 @@ __global__ void __launch_bounds__(NTHR, PF_FUSED_MINB)
         auto lo = rawq(k, c0, r0), hi = rawq(k, c1, r1);
         lo.Mv[0] = S.M[0][r0][c0]; lo.Mv[1] = S.M[1][r0][c0];
         hi.Mv[0] = S.M[0][r1][c1]; hi.Mv[1] = S.M[1][r1][c1];
-        mu_face_t<true, true>(kp, lo, hi, d, f);
+        mu_face_t<true, kFRoll>(kp, lo, hi, d, f);
         if (d == 0) { S.fx[0][r0 - 1][kFShfl ? 0 : TX] = f[0]; S.fx[1][r0 - 1][kFShfl ? 0 : TX] = f[1]; }
         else { S.fy[0][TY][c0 - 1] = f[0]; S.fy[1][TY][c0 - 1] = f[1]; }
       }

@@ -59,11 +59,14 @@ struct __align__(128) MuSmem {
 #define PF_MU_UNROLL 4
 #endif
 #ifndef PF_MU_ROLL
-#define PF_MU_ROLL 1
+#define PF_MU_ROLL 0
 #endif
-// x/y faces (both cells in shared memory): the three solids of the
-// anti-trapping current in a loop that is not unrolled — a third of the
-// code (measured on the all-guards-open state: 13.6 -> 10.8 ms; C4 unchanged)
+// x/y faces (both cells in shared memory): PF_MU_ROLL = 1 puts the three
+// solids of the anti-trapping current in a loop that is not unrolled — a
+// third of the code (measured on the all-guards-open state, round 2: 13.6 ->
+// 10.8 ms; C4 unchanged).  With the x faces by shuffle and the two-plane lead
+// the unrolled solids measured faster on both states (C4 2.960 -> 2.933 ms,
+// all-guards-open 9.86 -> 9.39 ms): 0 is the default
 constexpr bool kMuRoll = PF_MU_ROLL != 0;
 constexpr int kMuUnroll = PF_MU_UNROLL;   // plane-loop unroll (round 1: 2 -> 4 -0.8 %; with the rolled anti-trapping
                                           // solids and the library-call fallback, 4 spilled: C4 3.78 vs 3.15 ms; without
