@@ -13,6 +13,7 @@
 // own value only) comes from global memory one plane ahead.  One CTA barrier
 // per plane.  The face and gradient routines are the pinned ones of pf_dev.cuh:
 // a face evaluated at a tile / chunk / block edge has the same bits as mid-tile.
+#include <type_traits>
 #include "pf_kernels.cuh"
 #define PF_TILE_X PHI_TILE_X
 #define PF_TILE_Y PHI_TILE_Y
@@ -29,6 +30,12 @@ namespace pf {
 // fits 5 CTAs per SM at 96 registers: measured 3.68 ms vs 3.55 at 512^3, 3.78
 // at 4 CTAs — the shorter lead costs more than the occupancy gains)
 constexpr int PNS = PF_PHI_NS;
+#ifndef PF_PHI_FAR_SPLIT
+#define PF_PHI_FAR_SPLIT 1
+#endif
+#ifndef PF_PHI_FAR_SPLIT_ISO
+#define PF_PHI_FAR_SPLIT_ISO 0
+#endif
 template <bool ANISO>
 struct __align__(128) PhiSmemT {
   double p[PNS][NPH][TSZ];         // phi^n tile planes, (row, col) at row * RX + col
@@ -203,8 +210,34 @@ __global__ void __launch_bounds__(NTHR, ANISO ? PF_PHI_MINB : PF_PHI_MINB_ISO)
       // far faces: +y of the last row, +x of the last column (warp 0); the
       // isotropic kernel issues them first, the anisotropic one after its own
       // faces (measured: iso -1.1 %, aniso +5 % the other way round)
+      // PF_PHI_FAR_SPLIT (anisotropic): +y far faces on warp 0, +x far faces on
+      // warp 1, each with a compile-time direction (no run-time-d arrays in
+      // local memory — the kernel's 48-byte stack frame — no direction selects):
+      // C5-model phi 6.113 -> 5.944 ms at 512^3, bitwise the same fields; the
+      // isotropic face has no direction-dependent operands and measured slower
+      // split (3.64 vs 3.55 ms: PF_PHI_FAR_SPLIT_ISO off)
+      auto far_face_d = [&](auto dc, int c0, int r0) {
+        constexpr int d = decltype(dc)::value;
+        const int c1 = d == 1 ? c0 : c0 + 1, r1 = d == 1 ? r0 + 1 : r0;
+#pragma unroll
+        for (int a = 0; a < NPH; ++a) { lo[a] = T(S.p[sc][a], r0, c0); hi[a] = T(S.p[sc][a], r1, c1); }
+        if (ANISO) {
+          tan_grad(sc, sm, sp, c0, r0, d, gl);
+          tan_grad(sc, sm, sp, c1, r1, d, gh);
+        }
+        phi_face<PF_AN>(kp, lo, hi, ANISO ? gl : gdum, ANISO ? gh : gdum, d, jf);
+#pragma unroll
+        for (int a = 0; a < NPH; ++a) {
+          if (d == 0) S.fx[fb][a][r0 - 1][TX] = jf[a];
+          else S.fy[fb][a][TY][c0 - 1] = jf[a];
+        }
+      };
       auto far_faces = [&]() {
-        if (tid < TX + TY) {
+        if ((ANISO && PF_PHI_FAR_SPLIT) || (!ANISO && PF_PHI_FAR_SPLIT_ISO)) {
+          const int w = tid >> 5, l = tid & 31;
+          if (w == 0 && l < TX) far_face_d(std::integral_constant<int, 1>{}, l + 1, TY);
+          else if (w == 1 && l < TY) far_face_d(std::integral_constant<int, 0>{}, TX, l + 1);
+        } else if (tid < TX + TY) {
           const int d = tid < TX ? 1 : 0;
           const int c0 = d == 1 ? tid + 1 : TX, r0 = d == 1 ? TY : tid - TX + 1;
           const int c1 = d == 1 ? c0 : c0 + 1, r1 = d == 1 ? r0 + 1 : r0;
