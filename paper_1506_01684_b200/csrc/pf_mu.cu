@@ -20,6 +20,7 @@
 // in registers; the own column's phi^n / mu at k+1 (the z-face's upper cell)
 // come from registers.  All arithmetic is the pinned code of pf_dev.cuh, so
 // results do not depend on tile or block boundaries.
+#include <type_traits>
 #include "pf_kernels.cuh"
 #define PF_TILE_X MU_TILE_X
 #define PF_TILE_Y MU_TILE_Y
@@ -42,6 +43,10 @@ constexpr int NPM = PF_MU_PM_SLOTS;
 #define PF_MU_SHFL 1
 #endif
 constexpr bool kShfl = PF_MU_SHFL != 0 && TX == 32;
+// (measured: C4 2.958 vs 2.933 ms, all-guards-open 9.37 vs 9.39: off by default)
+#ifndef PF_MU_FAR_CONST
+#define PF_MU_FAR_CONST 0
+#endif
 
 struct __align__(128) MuSmem {
   double pn[NSLOT][NPH][TSZ];     // phi^{n+1}, planes k-1 .. k+2
@@ -364,7 +369,23 @@ __global__ void __launch_bounds__(NTHR, 512 / NTHR) mu_tiled_kernel(const __grid
         S.fy[0][ty][tx] = fyo[0];
         S.fy[1][ty][tx] = fyo[1];
       }
-      if (tid < TX + TY) {  // far faces: +y of the last row (warp 0), +x of the last column (warp 1)
+      // far faces: +y of the last row (warp 0), +x of the last column (warp 1);
+      // PF_MU_FAR_CONST: each with a compile-time direction (the face routine's
+      // component and accessor selects fold away)
+      auto far_face = [&](auto dc, int c0, int r0) {
+        constexpr int d = decltype(dc)::value;
+        const int c1 = d == 1 ? c0 : c0 + 1, r1 = d == 1 ? r0 + 1 : r0;
+        RawQ lo = rawq(k, c0, r0), hi = rawq(k, c1, r1);
+        lo.Mv[0] = S.M[0][r0][c0]; lo.Mv[1] = S.M[1][r0][c0];
+        hi.Mv[0] = S.M[0][r1][c1]; hi.Mv[1] = S.M[1][r1][c1];
+        mu_face_t<MODE == MU_FULL, kMuRoll>(kp, lo, hi, d, f);
+        if (d == 0) { FX_FAR(0, r0 - 1) = f[0]; FX_FAR(1, r0 - 1) = f[1]; }
+        else { S.fy[0][TY][c0 - 1] = f[0]; S.fy[1][TY][c0 - 1] = f[1]; }
+      };
+      if (PF_MU_FAR_CONST) {
+        if (tid < TX) far_face(std::integral_constant<int, 1>{}, tid + 1, TY);
+        else if (tid < TX + TY) far_face(std::integral_constant<int, 0>{}, TX, tid - TX + 1);
+      } else if (tid < TX + TY) {
         const int d = tid < TX ? 1 : 0;
         const int c0 = d == 1 ? tid + 1 : TX, r0 = d == 1 ? TY : tid - TX + 1;
         const int c1 = d == 1 ? c0 : c0 + 1, r1 = d == 1 ? r0 + 1 : r0;
