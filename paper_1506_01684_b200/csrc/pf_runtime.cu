@@ -1089,10 +1089,10 @@ pf_status pf_create(const pf_grid *g, const pf_params *p, pf_ctx **out) {
     kp.gf2[q] = kp.g2[q] * 0.5 / p->dx;
     kp.g2c[q] = kp.g2[q] * kp.inv_2dx * kp.inv_2dx;
     kp.omp[q] = 16.0 / (M_PI * M_PI) * p->gamma[pair_a(q)][pair_b(q)];
-    kp.delta[q] = p->aniso ? p->delta[pair_a(q)][pair_b(q)] : 0.0;
+    kp.delta16[q] = p->aniso ? 16.0 * p->delta[pair_a(q)][pair_b(q)] : 0.0;
   }
   kp.dmask = 0;
-  for (int q = 0; q < 6; ++q) kp.dmask |= (kp.delta[q] != 0.0 ? 1 : 0) << q;
+  for (int q = 0; q < 6; ++q) kp.dmask |= (kp.delta16[q] != 0.0 ? 1 : 0) << q;
   kp.pi_eps_16dt = M_PI * p->eps / (16.0 * p->dt);
   kp.Gv = p->G * p->v;
   kp.aniso = p->aniso ? 1 : 0;

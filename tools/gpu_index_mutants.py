@@ -28,8 +28,8 @@ MUTANTS = [
     ("relaxation time tau of phase 0 for every phase",
      "kp.dt_taueps[a] = p->dt / (p->tau[a] * p->eps);", "kp.dt_taueps[a] = p->dt / (p->tau[0] * p->eps);"),
     ("anisotropy delta_ab read as delta_a,l",
-     "kp.delta[q] = p->aniso ? p->delta[pair_a(q)][pair_b(q)] : 0.0;",
-     "kp.delta[q] = p->aniso ? p->delta[pair_a(q)][3] : 0.0;"),
+     "kp.delta16[q] = p->aniso ? 16.0 * p->delta[pair_a(q)][pair_b(q)] : 0.0;",
+     "kp.delta16[q] = p->aniso ? 16.0 * p->delta[pair_a(q)][3] : 0.0;"),
     ("diffusivity of component 0 for both components",
      "tp.D[a][q] = p->D[a][q];", "tp.D[a][q] = p->D[a][0];"),
     ("A1 of component 0 for both components",
